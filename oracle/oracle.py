@@ -1,0 +1,282 @@
+"""ctypes front-end for the oracles.  TEST INFRASTRUCTURE ONLY.
+
+Two checkers live here, both CPU:
+
+* ``port``      -- oracle/hetreco_oracle.c, the plain-C restatement of the
+                   reference kernels and FFT plan (liboracle.so, built by
+                   ``build()``; rebuilt on demand from the committed C source,
+                   so it also works on the GPU box).
+* ``reference`` -- oracle/_ref/libhetreco_refdrv.so, the reference library
+                   itself compiled from /root/reference by build_ref.sh and
+                   driven through its own ComputeSession API (ref_driver.cpp).
+
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
+``--impl reference`` legs may import this module.  Arrays follow the
+reference's column-major convention: a numpy array in Fortran order whose
+``shape`` equals the reference ``dims`` (ndarray.hpp:61-67).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+import threading
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+PORT_SO = os.path.join(HERE, "liboracle.so")
+REF_SO = os.path.join(HERE, "_ref", "libhetreco_refdrv.so")
+
+# ElementType codes: include/hetreco/ndarray.hpp:17-24 (wire format)
+UINT8, INT32, FLOAT32, COMPLEX64, FLOAT64, COMPLEX128 = 1, 2, 3, 4, 5, 6
+NP_OF_CODE = {UINT8: np.uint8, INT32: np.int32, FLOAT32: np.float32,
+              COMPLEX64: np.complex64, FLOAT64: np.float64, COMPLEX128: np.complex128}
+CODE_OF_NP = {np.dtype(v): k for k, v in NP_OF_CODE.items()}
+
+_lock = threading.Lock()
+_port = None
+_ref = None
+
+_vp, _u64, _f32, _f64, _i32 = C.c_void_p, C.c_uint64, C.c_float, C.c_double, C.c_int
+
+
+def build_port(force: bool = False) -> str:
+    """Compile the C restatement (gcc is in the image, here and on the box)."""
+    src = os.path.join(HERE, "hetreco_oracle.c")
+    if force or not os.path.exists(PORT_SO) or os.path.getmtime(PORT_SO) < os.path.getmtime(src):
+        tmp = PORT_SO + ".%d.tmp" % os.getpid()
+        subprocess.check_call(["gcc", "-O2", "-ffp-contract=off", "-fPIC", "-shared",
+                               "-o", tmp, src, "-lm"])
+        os.replace(tmp, PORT_SO)
+    return PORT_SO
+
+
+def build_reference() -> bool:
+    """Build oracle/_ref from /root/reference when present.  False if absent."""
+    if not os.path.isdir(os.environ.get("HETRECO_REFERENCE", "/root/reference")):
+        return os.path.exists(REF_SO)
+    subprocess.check_call([os.path.join(HERE, "build_ref.sh")])
+    return True
+
+
+def port():
+    global _port
+    with _lock:
+        if _port is None:
+            lib = C.CDLL(build_port())
+            lib.oracle_negate_u8.argtypes = [_vp, _vp, _u64, _f64]
+            lib.oracle_negate_f32.argtypes = [_vp, _vp, _u64, _f64]
+            lib.oracle_fft_radix2_pass.argtypes = [_vp, _vp, _u64, C.c_uint32, _u64, _u64, _u64,
+                                                   _f32, _vp]
+            lib.oracle_fft2d.argtypes = [_vp, _vp, _u64, _u64, _u64, _i32]
+            lib.oracle_complex_element_prod.argtypes = [_vp, _u64, _vp, _u64, _vp, _i32]
+            lib.oracle_ximage_sum.argtypes = [_vp, _vp, _u64, _u64, _u64]
+            lib.oracle_rss_combine.argtypes = [_vp, _vp, _u64, _u64, _u64]
+            lib.oracle_matrix_add_f32.argtypes = [_vp, _vp, _vp, _u64]
+            lib.oracle_sens_recon.argtypes = [_vp, _vp, _vp, _u64, _u64, _u64, _u64, _vp]
+            lib.oracle_rss_recon.argtypes = [_vp, _vp, _u64, _u64, _u64, _u64, _vp]
+            _port = lib
+        return _port
+
+
+def reference_available() -> bool:
+    return os.path.exists(REF_SO)
+
+
+def reference():
+    global _ref
+    with _lock:
+        if _ref is None:
+            if not os.path.exists(REF_SO):
+                raise RuntimeError("oracle/_ref not built (needs /root/reference at build time)")
+            lib = C.CDLL(REF_SO)
+            lib.refdrv_last_error.restype = C.c_char_p
+            lib.refdrv_run_kernel.argtypes = [C.c_char_p, _i32, _i32, _vp, _vp, _i32, _i32, _vp,
+                                              _vp, _i32, _i32, _vp, _vp, _i32, _vp, _u64, _u64]
+            lib.refdrv_fft2d.argtypes = [_vp, _vp, _u64, _u64, _u64, _i32]
+            lib.refdrv_recon.argtypes = [_i32, _vp, _vp, _vp, _u64, _u64, _u64, _u64, _i32,
+                                         C.POINTER(_f64), C.POINTER(_f64)]
+            lib.refdrv_layout_header.argtypes = [_i32, _vp, _vp, _vp, _u64, _vp, C.POINTER(_u64)]
+            _ref = lib
+        return _ref
+
+
+def _p(a: np.ndarray):
+    return C.c_void_p(a.ctypes.data)
+
+
+def _f(a, dtype) -> np.ndarray:
+    return np.asfortranarray(np.asarray(a, dtype=dtype))
+
+
+def _check_ref(rc):
+    if rc != 0:
+        raise RuntimeError("reference: " + reference().refdrv_last_error().decode())
+
+
+# ---------------------------------------------------------------------------
+# port (C restatement)
+# ---------------------------------------------------------------------------
+
+def negate(x: np.ndarray, max_value: float) -> np.ndarray:
+    x = np.asfortranarray(x)
+    out = np.empty_like(x, order="F")
+    if x.dtype == np.uint8:
+        port().oracle_negate_u8(_p(x), _p(out), x.size, float(max_value))
+    elif x.dtype == np.float32:
+        port().oracle_negate_f32(_p(x), _p(out), x.size, float(max_value))
+    else:
+        raise TypeError(x.dtype)
+    return out
+
+
+def fft_radix2_pass(data_in, data_out, mode, L, S, m, scale, payload: np.ndarray) -> np.ndarray:
+    """One reference pass; returns the updated copy of data_out."""
+    out = _f(data_out, np.complex64).copy(order="F")
+    din = _f(data_in, np.complex64) if data_in is not None else out
+    pl = np.ascontiguousarray(payload)
+    port().oracle_fft_radix2_pass(_p(din), _p(out), out.size, mode, L, S, m, float(scale), _p(pl))
+    return out
+
+
+def fft2d(x: np.ndarray, inverse: bool) -> np.ndarray:
+    x = _f(x, np.complex64)
+    nx, ny = x.shape[0], (x.shape[1] if x.ndim > 1 else 1)
+    batch = x.size // (nx * ny)
+    out = np.empty_like(x, order="F")
+    if port().oracle_fft2d(_p(x), _p(out), nx, ny, batch, int(bool(inverse))) != 0:
+        raise ValueError("fft2d: dims must be powers of two")
+    return out
+
+
+def complex_element_prod(x, s, conjugate: bool) -> np.ndarray:
+    x = _f(x, np.complex64)
+    s = _f(s, np.complex64)
+    out = np.empty_like(x, order="F")
+    port().oracle_complex_element_prod(_p(x), x.size, _p(s), s.size, _p(out), int(conjugate))
+    return out
+
+
+def ximage_sum(x) -> np.ndarray:
+    x = _f(x, np.complex64)
+    nx, ny, nc = x.shape[:3]
+    nf = x.size // (nx * ny * nc)
+    out = np.empty((nx, ny) + x.shape[3:], np.complex64, order="F")
+    port().oracle_ximage_sum(_p(x), _p(out), nx * ny, nc, nf)
+    return out
+
+
+def rss_combine(x) -> np.ndarray:
+    x = _f(x, np.complex64)
+    nx, ny, nc = x.shape[:3]
+    nf = x.size // (nx * ny * nc)
+    out = np.empty((nx, ny) + x.shape[3:], np.float32, order="F")
+    port().oracle_rss_combine(_p(x), _p(out), nx * ny, nc, nf)
+    return out
+
+
+def matrix_add(a, b) -> np.ndarray:
+    a = _f(a, np.float32)
+    b = _f(b, np.float32)
+    out = np.empty_like(a, order="F")
+    port().oracle_matrix_add_f32(_p(a), _p(b), _p(out), a.size)
+    return out
+
+
+def sens_recon(Y, S) -> np.ndarray:
+    Y = _f(Y, np.complex64)
+    S = _f(S, np.complex64)
+    nx, ny, nc, nf = (Y.shape + (1,))[:4]
+    M = np.empty((nx, ny, nf), np.complex64, order="F")
+    scratch = np.empty(2 * Y.size, np.complex64)
+    if port().oracle_sens_recon(_p(Y), _p(S), _p(M), nx, ny, nc, nf, _p(scratch)) != 0:
+        raise ValueError("sens_recon: dims must be powers of two")
+    return M
+
+
+def rss_recon(Y) -> np.ndarray:
+    Y = _f(Y, np.complex64)
+    nx, ny, nc, nf = (Y.shape + (1,))[:4]
+    R = np.empty((nx, ny, nf), np.float32, order="F")
+    scratch = np.empty(Y.size, np.complex64)
+    if port().oracle_rss_recon(_p(Y), _p(R), nx, ny, nc, nf, _p(scratch)) != 0:
+        raise ValueError("rss_recon: dims must be powers of two")
+    return R
+
+
+# ---------------------------------------------------------------------------
+# reference (the real library, oracle/_ref)
+# ---------------------------------------------------------------------------
+
+def _dims(a: np.ndarray):
+    d = np.array(a.shape if a.ndim else (1,), dtype=np.uint64)
+    return d, len(d)
+
+
+def ref_run_kernel(name: str, x: np.ndarray, params: bytes, gsize: int, out_like=None,
+                   extra: np.ndarray | None = None, in_place: bool = False) -> np.ndarray:
+    """Run one builtin kernel through ComputeSession::launch_kernel."""
+    x = np.asfortranarray(x)
+    xd, xr = _dims(x)
+    if extra is not None:
+        extra = np.asfortranarray(extra)
+        ed, er = _dims(extra)
+        et = CODE_OF_NP[extra.dtype]
+    else:
+        ed, er, et = np.zeros(1, np.uint64), 0, 0
+    if in_place:
+        out = x.copy(order="F")
+    else:
+        out = np.zeros_like(out_like, order="F") if out_like is not None else np.zeros_like(x)
+    od, orank = _dims(out)
+    pb = np.frombuffer(bytes(params) or b"\0", np.uint8).copy()
+    _check_ref(reference().refdrv_run_kernel(
+        name.encode(), CODE_OF_NP[x.dtype], xr, _p(xd), _p(x), et, er, _p(ed),
+        _p(extra) if extra is not None else None, CODE_OF_NP[out.dtype], orank, _p(od), _p(out),
+        int(in_place), _p(pb), len(params), gsize))
+    return out
+
+
+def ref_fft2d(x: np.ndarray, inverse: bool) -> np.ndarray:
+    x = _f(x, np.complex64)
+    nx, ny = x.shape[0], x.shape[1]
+    out = np.empty_like(x, order="F")
+    _check_ref(reference().refdrv_fft2d(_p(x), _p(out), nx, ny, x.size // (nx * ny),
+                                        int(bool(inverse))))
+    return out
+
+
+def ref_recon(method: str, Y: np.ndarray, S: np.ndarray | None = None, reps: int = 1):
+    """Returns (result, mean_seconds_per_launch, init_seconds)."""
+    Y = _f(Y, np.complex64)
+    nx, ny, nc, nf = (Y.shape + (1,))[:4]
+    if method == "sens":
+        S = _f(S, np.complex64)
+        out = np.empty((nx, ny, nf), np.complex64, order="F")
+    else:
+        out = np.empty((nx, ny, nf), np.float32, order="F")
+    mean_s, init_s = C.c_double(), C.c_double()
+    _check_ref(reference().refdrv_recon(0 if method == "sens" else 1, _p(Y),
+                                        _p(S) if S is not None else None, _p(out), nx, ny, nc,
+                                        nf, reps, C.byref(mean_s), C.byref(init_s)))
+    return out, mean_s.value, init_s.value
+
+
+def ref_pool_threads() -> int:
+    return int(reference().refdrv_pool_threads())
+
+
+def ref_layout_header(arrays, alignment: int = 256):
+    """arrays: list of (type_code, dims).  Returns (u64 words, total_bytes)."""
+    n = len(arrays)
+    types = np.array([t for t, _ in arrays], np.int32)
+    ranks = np.array([len(d) for _, d in arrays], np.int32)
+    dims8 = np.ones((n, 8), np.uint64)
+    for i, (_, d) in enumerate(arrays):
+        dims8[i, :len(d)] = d
+    words = np.zeros(1 + 11 * n, np.uint64)
+    total = C.c_uint64()
+    _check_ref(reference().refdrv_layout_header(n, _p(types), _p(ranks), _p(dims8), alignment,
+                                                _p(words), C.byref(total)))
+    return words, total.value
