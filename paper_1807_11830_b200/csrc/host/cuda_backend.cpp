@@ -1,0 +1,336 @@
+// cuda_backend.cpp -- the Backend contract (reference include/hetreco/
+// backend.hpp:44-79) implemented on one B200, plus the process-wide backend
+// list (backend.cpp:294-323 role) and the kernel registry (kernels.cpp).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <set>
+
+#include "../kernels/launch.hpp"
+#include "hetreco_b200/runtime.hpp"
+
+namespace hetreco {
+
+namespace {
+
+[[noreturn]] void raise_cuda(cudaError_t e, const std::string& what) {
+    if (e == cudaErrorMemoryAllocation) throw AllocationFailure(what + ": " + cudaGetErrorString(e));
+    throw Error(what + ": " + cudaGetErrorString(e));
+}
+
+void ck(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) raise_cuda(e, what);
+}
+
+// Host entry point stored in CompiledKernel::fn for device kernels: the
+// registry requires a non-null fn (kernels.cpp:13), but these kernels only
+// run on the GPU, so a host call is an error, never a silent CPU fallback.
+void device_only_entry(const hetreco_kernel_args*, std::uint64_t, std::uint64_t) {
+    throw DeviceError("<device kernel>", "sm_100a kernels cannot be invoked on the host");
+}
+
+void check_window(const char* what, std::uint64_t off, std::uint64_t len, std::uint64_t size) {
+    if (off > size || len > size - off)
+        throw InvalidArgument(std::string(what) + " window [" + std::to_string(off) + ", " +
+                              std::to_string(off + len) + ") exceeds buffer size " + std::to_string(size));
+}
+
+}  // namespace
+
+int cuda_device_count() {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return n;
+}
+
+// ---- CudaBackend ------------------------------------------------------------------------
+
+CudaBackend::CudaBackend(int ordinal, std::uint64_t capacity) : ordinal_(ordinal), capacity_(capacity) {
+    id_ = "cuda" + std::to_string(ordinal);
+    cudaDeviceProp p{};
+    ck(cudaGetDeviceProperties(&p, ordinal), "cudaGetDeviceProperties");
+    desc_.backend_id = id_;
+    desc_.device_index = 0;
+    desc_.device_type = DeviceType::Gpu;
+    desc_.vendor = "NVIDIA";
+    desc_.name = p.name;
+    desc_.api_version = std::to_string(p.major) + "." + std::to_string(p.minor);
+    desc_.global_memory_bytes = capacity ? capacity : std::uint64_t(p.totalGlobalMem);
+    desc_.base_alignment_bytes = 256;
+    desc_.supports_source_kernels = false;
+    make_current();
+    ck(cudaStreamCreateWithFlags(&compute_, cudaStreamNonBlocking), "cudaStreamCreate");
+    ck(cudaStreamCreateWithFlags(&h2d_, cudaStreamNonBlocking), "cudaStreamCreate");
+    ck(cudaStreamCreateWithFlags(&d2h_, cudaStreamNonBlocking), "cudaStreamCreate");
+    ck(cudaEventCreateWithFlags(&ev_compute_, cudaEventDisableTiming), "cudaEventCreate");
+    ck(cudaEventCreateWithFlags(&ev_copy_, cudaEventDisableTiming), "cudaEventCreate");
+    ring_size_ = 1u << 20;
+    ck(cudaHostAlloc(reinterpret_cast<void**>(&ring_host_), ring_size_, cudaHostAllocDefault), "cudaHostAlloc");
+    ck(cudaMalloc(reinterpret_cast<void**>(&ring_dev_), ring_size_), "cudaMalloc");
+}
+
+CudaBackend::~CudaBackend() {
+    cudaSetDevice(ordinal_);
+    cudaStreamSynchronize(compute_);
+    for (auto& [id, b] : bufs_) cudaFree(b.ptr);
+    cudaFree(ring_dev_);
+    cudaFreeHost(ring_host_);
+    cudaEventDestroy(ev_compute_);
+    cudaEventDestroy(ev_copy_);
+    cudaStreamDestroy(compute_);
+    cudaStreamDestroy(h2d_);
+    cudaStreamDestroy(d2h_);
+}
+
+void CudaBackend::make_current() const { ck(cudaSetDevice(ordinal_), "cudaSetDevice"); }
+
+const CudaBackend::Buf& CudaBackend::lookup(BufferId id) const {
+    auto it = bufs_.find(id);
+    if (it == bufs_.end()) throw UnknownHandle("unknown buffer " + std::to_string(id));
+    return it->second;
+}
+
+BufferId CudaBackend::allocate(std::uint64_t bytes) {
+    std::lock_guard lk(mu_);
+    if (capacity_ && (bytes > capacity_ || used_ > capacity_ - bytes))
+        throw AllocationFailure("allocation of " + std::to_string(bytes) + " bytes exceeds device capacity (" +
+                                std::to_string(capacity_ - used_) + " of " + std::to_string(capacity_) +
+                                " bytes free)");
+    make_current();
+    void* p = nullptr;
+    const cudaError_t e = cudaMalloc(&p, bytes ? bytes : 1);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        throw AllocationFailure("cudaMalloc of " + std::to_string(bytes) + " bytes failed: " + cudaGetErrorString(e));
+    }
+    // zero-filled like the reference's buffers (backend.cpp:137-141), in queue order
+    ck(cudaMemsetAsync(p, 0, bytes ? bytes : 1, compute_), "cudaMemsetAsync");
+    const BufferId id = next_++;
+    bufs_.emplace(id, Buf{p, bytes});
+    used_ += bytes;
+    return id;
+}
+
+void CudaBackend::release(BufferId id) {
+    std::lock_guard lk(mu_);
+    auto it = bufs_.find(id);
+    if (it == bufs_.end()) throw UnknownHandle("release of unknown buffer " + std::to_string(id));
+    make_current();
+    cudaStreamSynchronize(compute_);  // in-flight kernels may still read it
+    cudaFree(it->second.ptr);
+    used_ -= it->second.size;
+    bufs_.erase(it);
+}
+
+void CudaBackend::upload(BufferId id, std::uint64_t off, std::span<const std::byte> bytes) {
+    std::lock_guard lk(mu_);
+    const Buf& b = lookup(id);
+    check_window("upload", off, bytes.size(), b.size);
+    if (bytes.empty()) return;
+    make_current();
+    ck(cudaMemcpyAsync(static_cast<char*>(b.ptr) + off, bytes.data(), bytes.size(), cudaMemcpyHostToDevice,
+                       compute_),
+       "cudaMemcpyAsync(H2D)");
+    const cudaError_t e = cudaStreamSynchronize(compute_);  // host span is borrowed
+    if (e != cudaSuccess) throw DeviceError(last_kernel_.empty() ? "<upload>" : last_kernel_, cudaGetErrorString(e));
+}
+
+void CudaBackend::download(BufferId id, std::uint64_t off, std::span<std::byte> into) const {
+    std::lock_guard lk(mu_);
+    const Buf& b = lookup(id);
+    check_window("download", off, into.size(), b.size);
+    if (into.empty()) return;
+    make_current();
+    ck(cudaMemcpyAsync(into.data(), static_cast<const char*>(b.ptr) + off, into.size(), cudaMemcpyDeviceToHost,
+                       compute_),
+       "cudaMemcpyAsync(D2H)");
+    const cudaError_t e = cudaStreamSynchronize(compute_);
+    if (e != cudaSuccess) throw DeviceError(last_kernel_.empty() ? "<download>" : last_kernel_, cudaGetErrorString(e));
+}
+
+void CudaBackend::copy(BufferId src, std::uint64_t so, BufferId dst, std::uint64_t doff, std::uint64_t n) {
+    std::lock_guard lk(mu_);
+    const Buf& s = lookup(src);
+    const Buf& d = lookup(dst);
+    check_window("copy source", so, n, s.size);
+    check_window("copy destination", doff, n, d.size);
+    if (src == dst && so < doff + n && doff < so + n)
+        throw InvalidArgument("overlapping copy within buffer " + std::to_string(src));
+    if (n == 0) return;
+    make_current();
+    ck(cudaMemcpyAsync(static_cast<char*>(d.ptr) + doff, static_cast<const char*>(s.ptr) + so, n,
+                       cudaMemcpyDeviceToDevice, compute_),
+       "cudaMemcpyAsync(D2D)");
+}
+
+std::vector<CompiledKernel> CudaBackend::intrinsic_kernels() {
+    std::vector<CompiledKernel> ks;
+    for (int i = 0; i < int(dev::Builtin::Count); ++i) {
+        const char* n = dev::builtin_name(dev::Builtin(i));
+        ks.push_back({n, std::string("sm_100a:") + n, &device_only_entry});
+    }
+    return ks;
+}
+
+std::vector<CompiledKernel> CudaBackend::compile(std::span<const ProgramSource>) {
+    throw UnsupportedSource("backend '" + id_ +
+                            "' runs precompiled sm_100a kernels and cannot compile kernel source");
+}
+
+void* CudaBackend::stage_params(std::span<const std::byte> params) {
+    const std::uint64_t need = std::max<std::uint64_t>(256, (params.size() + 255) & ~std::uint64_t(255));
+    if (need > ring_size_) {
+        ck(cudaStreamSynchronize(compute_), "cudaStreamSynchronize");
+        cudaFree(ring_dev_);
+        cudaFreeHost(ring_host_);
+        ring_size_ = need * 2;
+        ck(cudaHostAlloc(reinterpret_cast<void**>(&ring_host_), ring_size_, cudaHostAllocDefault), "cudaHostAlloc");
+        ck(cudaMalloc(reinterpret_cast<void**>(&ring_dev_), ring_size_), "cudaMalloc");
+        ring_head_ = 0;
+    }
+    if (ring_head_ + need > ring_size_) {
+        // every earlier staging copy is consumed once the queue drains
+        ck(cudaStreamSynchronize(compute_), "cudaStreamSynchronize");
+        ring_head_ = 0;
+    }
+    std::byte* h = ring_host_ + ring_head_;
+    std::byte* d = ring_dev_ + ring_head_;
+    if (!params.empty()) std::memcpy(h, params.data(), params.size());
+    ck(cudaMemcpyAsync(d, h, need, cudaMemcpyHostToDevice, compute_), "cudaMemcpyAsync(params)");
+    ring_head_ += need;
+    return d;
+}
+
+void CudaBackend::execute(const CompiledKernel& kernel, const KernelBinding& bind, std::uint64_t gsize) {
+    std::lock_guard lk(mu_);
+    const int which = dev::builtin_from_name(kernel.name.c_str());
+    if (which < 0) throw DeviceError(kernel.name, "no sm_100a implementation registered under this name");
+    hetreco_kernel_args args{};
+    args.in = lookup(bind.input).ptr;
+    args.in_layout = static_cast<const std::uint64_t*>(lookup(bind.input_header).ptr);
+    args.out = lookup(bind.output).ptr;
+    args.out_layout = static_cast<const std::uint64_t*>(lookup(bind.output_header).ptr);
+    make_current();
+    args.params = stage_params(bind.params);
+    args.params_size = bind.params.size();
+    last_kernel_ = kernel.name;
+    const cudaError_t e = dev::launch_builtin(dev::Builtin(which), args, gsize, compute_);
+    if (e != cudaSuccess) throw DeviceError(kernel.name, cudaGetErrorString(e));
+}
+
+void CudaBackend::synchronize() {
+    make_current();
+    const cudaError_t e = cudaStreamSynchronize(compute_);
+    if (e != cudaSuccess) throw DeviceError(last_kernel_.empty() ? "<none>" : last_kernel_, cudaGetErrorString(e));
+}
+
+void CudaBackend::check(const char* what) const {
+    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaStreamQuery(compute_);
+    if (e != cudaSuccess && e != cudaErrorNotReady) throw DeviceError(what, cudaGetErrorString(e));
+}
+
+void* CudaBackend::device_pointer(BufferId id) const {
+    std::lock_guard lk(mu_);
+    return lookup(id).ptr;
+}
+
+std::uint64_t CudaBackend::buffer_size(BufferId id) const {
+    std::lock_guard lk(mu_);
+    return lookup(id).size;
+}
+
+std::uint64_t CudaBackend::live_bytes() const {
+    std::lock_guard lk(mu_);
+    return used_;
+}
+
+// ---- backend list ----------------------------------------------------------------------
+
+namespace {
+
+std::vector<std::unique_ptr<CudaBackend>>& owned() {
+    static std::vector<std::unique_ptr<CudaBackend>> list = [] {
+        std::vector<std::unique_ptr<CudaBackend>> v;
+        const int n = cuda_device_count();
+        for (int i = 0; i < n; ++i) v.push_back(std::make_unique<CudaBackend>(i));
+        return v;
+    }();
+    return list;
+}
+
+}  // namespace
+
+std::span<Backend* const> backend_snapshot() {
+    static const std::vector<Backend*> ptrs = [] {
+        std::vector<Backend*> v;
+        for (auto& b : owned()) v.push_back(b.get());
+        return v;
+    }();
+    return ptrs;
+}
+
+Backend& backend_by_id(std::string_view id) {
+    std::string known;
+    for (Backend* b : backend_snapshot()) {
+        if (b->id() == id) return *b;
+        known += (known.empty() ? "" : ", ") + std::string(b->id());
+    }
+    throw InvalidArgument("unknown backend '" + std::string(id) + "'; known backends: " +
+                          (known.empty() ? "(none)" : known));
+}
+
+// ---- kernel registry (kernels.cpp:8-50 semantics) ------------------------------------------
+
+void KernelRegistry::add(std::vector<CompiledKernel> ks) {
+    std::set<std::string> batch;
+    for (const CompiledKernel& k : ks) {
+        if (k.name.empty()) throw InvalidArgument("kernel with empty name in unit '" + k.unit_name + "'");
+        if (!k.fn) throw InvalidArgument("kernel '" + k.name + "' has no entry point");
+        if (!batch.insert(k.name).second)
+            throw DuplicateKernel("kernel '" + k.name + "' appears twice in one batch (unit '" + k.unit_name + "')");
+        if (auto it = table_.find(k.name); it != table_.end())
+            throw DuplicateKernel("kernel '" + k.name + "' from unit '" + k.unit_name +
+                                  "' is already registered (unit '" + it->second.unit_name + "')");
+    }
+    for (CompiledKernel& k : ks) {
+        std::string key = k.name;
+        table_.emplace(std::move(key), std::move(k));
+    }
+}
+
+const CompiledKernel& KernelRegistry::find(std::string_view name) const {
+    if (auto it = table_.find(name); it != table_.end()) return it->second;
+    std::string msg = "unknown kernel '" + std::string(name) + "'; registered:";
+    if (table_.empty()) msg += " (none)";
+    for (const auto& [k, v] : table_) msg += " " + k;
+    throw UnknownKernel(msg);
+}
+
+bool KernelRegistry::contains(std::string_view name) const { return table_.find(name) != table_.end(); }
+
+std::vector<std::string> KernelRegistry::names() const {
+    std::vector<std::string> v;
+    for (const auto& [k, x] : table_) v.push_back(k);
+    return v;
+}
+
+std::span<const ProgramSource> builtin_kernel_sources() {
+    // The builtins ship as precompiled sm_100a code (no source text to JIT);
+    // the units are listed by name so callers can enumerate them.
+    static const std::vector<ProgramSource> units = [] {
+        std::vector<ProgramSource> v;
+        for (int i = 0; i < int(dev::Builtin::Count); ++i) {
+            const std::string n = dev::builtin_name(dev::Builtin(i));
+            v.push_back({n + ".cu", "// precompiled sm_100a builtin '" + n + "'"});
+        }
+        return v;
+    }();
+    return units;
+}
+
+}  // namespace hetreco

@@ -1,0 +1,879 @@
+// processes.cpp -- Process / GraphProcess / CompositeProcess and the builtin
+// reconstruction processes (reference include/hetreco/process.hpp:21-140,
+// SPEC.md:293-477).
+#include "hetreco_b200/processes.hpp"
+
+#include <cuda_runtime.h>
+
+#include <chrono>
+#include <cmath>
+#include <cstring>
+
+#include "../kernels/launch.hpp"
+
+namespace hetreco {
+
+namespace {
+
+void ck(cudaError_t e, const std::string& what) {
+    if (e == cudaSuccess) return;
+    cudaGetLastError();
+    if (e == cudaErrorMemoryAllocation) throw AllocationFailure(what + ": " + cudaGetErrorString(e));
+    throw DeviceError(what, cudaGetErrorString(e));
+}
+
+bool is_pow2(std::uint64_t v) { return v && !(v & (v - 1)); }
+
+// Owning device allocation on the session's GPU.
+class DevMem {
+public:
+    DevMem() = default;
+    DevMem(std::uint64_t bytes) : size_(bytes) {
+        ck(cudaMalloc(&p_, bytes ? bytes : 1), "cudaMalloc(process scratch)");
+    }
+    ~DevMem() {
+        if (p_) cudaFree(p_);
+    }
+    DevMem(DevMem&& o) noexcept : p_(o.p_), size_(o.size_) { o.p_ = nullptr; }
+    DevMem& operator=(DevMem&& o) noexcept {
+        if (this != &o) {
+            if (p_) cudaFree(p_);
+            p_ = o.p_;
+            size_ = o.size_;
+            o.p_ = nullptr;
+        }
+        return *this;
+    }
+    void* get() const { return p_; }
+    template <class T>
+    T* as() const { return static_cast<T*>(p_); }
+    std::uint64_t size() const { return size_; }
+
+private:
+    void* p_ = nullptr;
+    std::uint64_t size_ = 0;
+};
+
+DevMem upload_bytes(const void* src, std::uint64_t n) {
+    DevMem m(n);
+    ck(cudaMemcpy(m.get(), src, n, cudaMemcpyHostToDevice), "cudaMemcpy(process constants)");
+    return m;
+}
+
+// W_N^t = exp(dir * 2 pi i t / N), t < N, computed in double, stored as float
+// (the reference bakes its pass payloads the same way, fft_radix2_pass.cl.src:15-16).
+DevMem twiddle_table(std::uint64_t N, int dir) {
+    std::vector<float> w(2 * std::max<std::uint64_t>(N, 1));
+    for (std::uint64_t t = 0; t < N; ++t) {
+        const double th = double(dir) * 2.0 * M_PI * double(t) / double(N);
+        w[2 * t] = float(std::cos(th));
+        w[2 * t + 1] = float(std::sin(th));
+    }
+    return upload_bytes(w.data(), w.size() * sizeof(float));
+}
+
+int sm_count(int ordinal) {
+    int n = 0;
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, ordinal) != cudaSuccess) n = 148;
+    return n;
+}
+
+std::uint64_t prod(const LayoutRecord& r, std::uint32_t from, std::uint32_t to) {
+    std::uint64_t n = 1;
+    for (std::uint32_t d = from; d < to && d < r.rank; ++d) n *= r.dims[d];
+    return n;
+}
+
+std::string dims_str(const LayoutRecord& r) {
+    std::string s = "[";
+    for (std::uint32_t d = 0; d < r.rank; ++d) s += (d ? "," : "") + std::to_string(r.dims[d]);
+    return s + "]";
+}
+
+const LayoutRecord& array_of(const LayoutDescriptor& l, std::size_t i, const std::string& who) {
+    if (i >= l.records.size())
+        throw ShapeMismatch(who + ": data set has " + std::to_string(l.records.size()) + " array(s), needs array " +
+                            std::to_string(i));
+    return l.records[i];
+}
+
+void require_type(const LayoutRecord& r, ElementType t, const std::string& who) {
+    if (r.element_type != t)
+        throw UnsupportedElementType(who + ": expected " + std::string(element_type_name(t)) + ", got " +
+                                     std::string(element_type_name(r.element_type)));
+}
+
+}  // namespace
+
+// ---- ProcessParams ----------------------------------------------------------------------
+
+ProcessParams& ProcessParams::set(std::string k, bool v) { values_[std::move(k)] = v; return *this; }
+ProcessParams& ProcessParams::set(std::string k, std::int64_t v) { values_[std::move(k)] = v; return *this; }
+ProcessParams& ProcessParams::set(std::string k, double v) { values_[std::move(k)] = v; return *this; }
+ProcessParams& ProcessParams::set(std::string k, std::string v) { values_[std::move(k)] = std::move(v); return *this; }
+
+const ProcessParams::Value* ProcessParams::find(std::string_view k) const {
+    auto it = values_.find(k);
+    return it == values_.end() ? nullptr : &it->second;
+}
+
+bool ProcessParams::has(std::string_view k) const { return find(k) != nullptr; }
+
+bool ProcessParams::get_bool(std::string_view k, bool fb) const {
+    const Value* v = find(k);
+    if (!v) return fb;
+    if (auto* b = std::get_if<bool>(v)) return *b;
+    throw InvalidParams("parameter '" + std::string(k) + "' is not a boolean");
+}
+
+std::int64_t ProcessParams::get_int(std::string_view k, std::int64_t fb) const {
+    const Value* v = find(k);
+    if (!v) return fb;
+    if (auto* i = std::get_if<std::int64_t>(v)) return *i;
+    throw InvalidParams("parameter '" + std::string(k) + "' is not an integer");
+}
+
+double ProcessParams::get_real(std::string_view k, double fb) const {
+    const Value* v = find(k);
+    if (!v) return fb;
+    if (auto* d = std::get_if<double>(v)) return *d;
+    if (auto* i = std::get_if<std::int64_t>(v)) return double(*i);  // integers promote
+    throw InvalidParams("parameter '" + std::string(k) + "' is not a real");
+}
+
+std::string ProcessParams::get_string(std::string_view k, std::string_view fb) const {
+    const Value* v = find(k);
+    if (!v) return std::string(fb);
+    if (auto* s = std::get_if<std::string>(v)) return *s;
+    throw InvalidParams("parameter '" + std::string(k) + "' is not a string");
+}
+
+void ProcessParams::require_known(std::initializer_list<std::string_view> known) const {
+    for (const auto& [k, v] : values_) {
+        bool ok = false;
+        for (auto q : known) ok = ok || q == k;
+        if (!ok) {
+            std::string allowed;
+            for (auto q : known) allowed += (allowed.empty() ? "" : ", ") + std::string(q);
+            throw InvalidParams("unknown parameter '" + k + "' (accepted: " + (allowed.empty() ? "none" : allowed) +
+                                ")");
+        }
+    }
+}
+
+// ---- Process ----------------------------------------------------------------------------
+
+struct Process::Timing {
+    static constexpr int kRing = 128;
+    int device = -1;
+    cudaStream_t stream = nullptr;
+    cudaEvent_t start[kRing]{}, stop[kRing]{};
+    int head = 0, pending = 0;
+};
+
+Process::Process(ComputeSession& s, std::string name) : session_(s), name_(std::move(name)) {}
+
+Process::~Process() {
+    if (timing_) {
+        cudaSetDevice(timing_->device);
+        for (int i = 0; i < Timing::kRing; ++i) {
+            if (timing_->start[i]) cudaEventDestroy(timing_->start[i]);
+            if (timing_->stop[i]) cudaEventDestroy(timing_->stop[i]);
+        }
+    }
+}
+
+void Process::set_input(DataHandle h) {
+    session_.layout_of(h);  // UnknownHandle for foreign/stale handles
+    if (state_ == ProcessState::Initialized && !(h == input_)) rebound_ = true;
+    input_ = h;
+}
+
+void Process::set_output(DataHandle h) {
+    session_.layout_of(h);
+    if (state_ == ProcessState::Initialized && !(h == output_)) rebound_ = true;
+    output_ = h;
+}
+
+DataHandle Process::require_input() const {
+    if (!input_.valid()) throw InvalidArgument("process '" + name_ + "' has no input handle");
+    return input_;
+}
+
+DataHandle Process::require_output() const {
+    if (!output_.valid()) throw InvalidArgument("process '" + name_ + "' has no output handle");
+    return output_;
+}
+
+void Process::init(const ProcessParams& params) {
+    if (state_ != ProcessState::Created) throw AlreadyInitialized("process '" + name_ + "' is already initialized");
+    const auto t0 = std::chrono::steady_clock::now();
+    on_init(params);
+    state_ = ProcessState::Initialized;
+    rebound_ = false;
+    stats_.init_calls += 1;
+    stats_.init_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
+
+void Process::launch() {
+    if (state_ != ProcessState::Initialized) throw NotInitialized("process '" + name_ + "' launched before init()");
+    if (rebound_) {
+        on_rebind();
+        rebound_ = false;
+    }
+    if (!timing_) {
+        timing_ = std::make_unique<Timing>();
+        CudaBackend& cb = session_.cuda();
+        timing_->device = cb.ordinal();
+        timing_->stream = cb.compute_stream();
+        cb.make_current();
+        for (int i = 0; i < Timing::kRing; ++i) {
+            ck(cudaEventCreate(&timing_->start[i]), "cudaEventCreate");
+            ck(cudaEventCreate(&timing_->stop[i]), "cudaEventCreate");
+        }
+    }
+    Timing& t = *timing_;
+    if (t.pending == Timing::kRing) resolve_timings();
+    const int slot = (t.head + t.pending) % Timing::kRing;
+    cudaSetDevice(t.device);
+    cudaEventRecord(t.start[slot], t.stream);
+    on_launch();
+    cudaEventRecord(t.stop[slot], t.stream);
+    t.pending += 1;
+    stats_.launches += 1;
+}
+
+void Process::resolve_timings() const {
+    if (!timing_) return;
+    Timing& t = *timing_;
+    cudaSetDevice(t.device);
+    while (t.pending > 0) {
+        const int s = t.head;
+        float ms = 0.f;
+        const cudaError_t e = cudaEventSynchronize(t.stop[s]);
+        if (e != cudaSuccess) {
+            t.pending = 0;
+            throw DeviceError(name_, cudaGetErrorString(e));
+        }
+        cudaEventElapsedTime(&ms, t.start[s], t.stop[s]);
+        stats_.last_launch_seconds = double(ms) * 1e-3;
+        stats_.total_launch_seconds += stats_.last_launch_seconds;
+        t.head = (t.head + 1) % Timing::kRing;
+        t.pending -= 1;
+    }
+}
+
+const LaunchStats& Process::stats() const {
+    resolve_timings();
+    return stats_;
+}
+
+// ---- GraphProcess -----------------------------------------------------------------------
+
+GraphProcess::~GraphProcess() {
+    if (exec_) cudaGraphExecDestroy(exec_);
+    if (graph_) cudaGraphDestroy(graph_);
+}
+
+void GraphProcess::on_init(const ProcessParams& params) {
+    params_ = params;
+    session().cuda().make_current();
+    bake(params);
+    capture();
+}
+
+void GraphProcess::on_rebind() {
+    session().cuda().make_current();
+    rebake();
+    capture();
+}
+
+void GraphProcess::capture() {
+    CudaBackend& cb = session().cuda();
+    cb.make_current();
+    cudaStream_t cs = nullptr;
+    ck(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking), "cudaStreamCreate");
+    cudaGraph_t g = nullptr;
+    ck(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal), "cudaStreamBeginCapture");
+    try {
+        record(cs);
+    } catch (...) {
+        cudaStreamEndCapture(cs, &g);
+        if (g) cudaGraphDestroy(g);
+        cudaStreamDestroy(cs);
+        throw;
+    }
+    const cudaError_t e = cudaStreamEndCapture(cs, &g);
+    cudaStreamDestroy(cs);
+    ck(e, "capture of process '" + name() + "'");
+    cudaGraphExec_t x = nullptr;
+    const cudaError_t ei = cudaGraphInstantiate(&x, g, 0);
+    if (ei != cudaSuccess) {
+        cudaGraphDestroy(g);
+        ck(ei, "cudaGraphInstantiate('" + name() + "')");
+    }
+    if (exec_) cudaGraphExecDestroy(exec_);
+    if (graph_) cudaGraphDestroy(graph_);
+    graph_ = g;
+    exec_ = x;
+    ck(cudaGraphUpload(exec_, cb.compute_stream()), "cudaGraphUpload");
+}
+
+void GraphProcess::mark(cudaStream_t s) {
+    if (!profiling_) return;
+    cudaEvent_t e = nullptr;
+    ck(cudaEventCreate(&e), "cudaEventCreate");
+    cudaEventRecord(e, s);
+    marks_.push_back(e);
+}
+
+std::vector<double> GraphProcess::profile(int reps) {
+    if (state() != ProcessState::Initialized) throw NotInitialized("process '" + name() + "' profiled before init()");
+    CudaBackend& cb = session().cuda();
+    cb.make_current();
+    cudaStream_t s = cb.compute_stream();
+    std::vector<double> acc;
+    profiling_ = true;
+    try {
+        for (int r = 0; r < reps; ++r) {
+            marks_.clear();
+            mark(s);
+            record(s);
+            ck(cudaStreamSynchronize(s), "profile(" + name() + ")");
+            if (acc.empty()) acc.assign(marks_.size() > 1 ? marks_.size() - 1 : 0, 0.0);
+            for (std::size_t i = 1; i < marks_.size() && i - 1 < acc.size(); ++i) {
+                float ms = 0.f;
+                cudaEventElapsedTime(&ms, marks_[i - 1], marks_[i]);
+                acc[i - 1] += double(ms) * 1e-3;
+            }
+            for (cudaEvent_t e : marks_) cudaEventDestroy(e);
+            marks_.clear();
+        }
+    } catch (...) {
+        profiling_ = false;
+        for (cudaEvent_t e : marks_) cudaEventDestroy(e);
+        marks_.clear();
+        throw;
+    }
+    profiling_ = false;
+    for (double& a : acc) a /= std::max(1, reps);
+    return acc;
+}
+
+void GraphProcess::on_launch() {
+    CudaBackend& cb = session().cuda();
+    const cudaError_t e = cudaGraphLaunch(exec_, cb.compute_stream());
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        throw DeviceError(name(), cudaGetErrorString(e));
+    }
+}
+
+// ---- CompositeProcess -------------------------------------------------------------------------
+
+CompositeProcess::CompositeProcess(ComputeSession& s, std::string name, std::vector<std::unique_ptr<Process>> stages)
+    : GraphProcess(s, std::move(name)), stages_(std::move(stages)) {
+    if (stages_.empty()) throw InvalidArgument("chain '" + this->name() + "' has no stages");
+    for (std::size_t i = 0; i < stages_.size(); ++i) {
+        if (!stages_[i]) throw InvalidArgument("chain stage " + std::to_string(i) + " is null");
+        if (&stages_[i]->session() != &s)
+            throw ChainMismatch("stage " + std::to_string(i) + " belongs to another session");
+        if (!dynamic_cast<GraphProcess*>(stages_[i].get())) all_graph_ = false;
+    }
+    for (std::size_t i = 0; i + 1 < stages_.size(); ++i) {
+        if (!(stages_[i]->output() == stages_[i + 1]->input()) || !stages_[i]->output().valid())
+            throw ChainMismatch("stage " + std::to_string(i) + " ('" + stages_[i]->name() +
+                                "') output is not the input of stage " + std::to_string(i + 1) + " ('" +
+                                stages_[i + 1]->name() + "')");
+    }
+    if (stages_.front()->input().valid()) set_input(stages_.front()->input());
+    if (stages_.back()->output().valid()) set_output(stages_.back()->output());
+}
+
+void CompositeProcess::bake(const ProcessParams& params) {
+    params.require_known({});
+    for (std::size_t i = 0; i < stages_.size(); ++i) {
+        try {
+            if (stages_[i]->state() == ProcessState::Created) stages_[i]->init();
+        } catch (const std::exception& e) {
+            throw ChainStageError(i, stages_[i]->name(), e.what());
+        }
+    }
+}
+
+void CompositeProcess::record(cudaStream_t s) {
+    for (std::size_t i = 0; i < stages_.size(); ++i) {
+        auto* g = dynamic_cast<GraphProcess*>(stages_[i].get());
+        if (!g) continue;  // non-graph stages launch one by one (on_launch)
+        try {
+            g->record(s);
+        } catch (const std::exception& e) {
+            throw ChainStageError(i, stages_[i]->name(), e.what());
+        }
+    }
+}
+
+void CompositeProcess::on_launch() {
+    if (all_graph_) {
+        GraphProcess::on_launch();
+        return;
+    }
+    for (std::size_t i = 0; i < stages_.size(); ++i) {
+        try {
+            stages_[i]->launch();
+        } catch (const std::exception& e) {
+            throw ChainStageError(i, stages_[i]->name(), e.what());
+        }
+    }
+}
+
+std::unique_ptr<CompositeProcess> chain(ComputeSession& s, std::string name, std::vector<std::unique_ptr<Process>> stages) {
+    return std::make_unique<CompositeProcess>(s, std::move(name), std::move(stages));
+}
+
+// ---- builtin processes ------------------------------------------------------------------------
+
+namespace {
+
+class NegateProcess final : public GraphProcess {
+public:
+    using GraphProcess::GraphProcess;
+    void bake(const ProcessParams& p) override {
+        p.require_known({"max_value"});
+        const LayoutRecord& ri = array_of(input_layout(), 0, name());
+        const LayoutRecord& ro = array_of(output_layout(), 0, name());
+        if (ri.element_type != ElementType::UInt8 && ri.element_type != ElementType::Float32)
+            throw UnsupportedElementType(name() + ": negate supports uint8 and float32, got " +
+                                         std::string(element_type_name(ri.element_type)));
+        if (ri.element_type != ro.element_type || ri.dims != ro.dims)
+            throw ShapeMismatch(name() + ": output " + dims_str(ro) + " does not match input " + dims_str(ri));
+        type_ = int(ri.element_type);
+        n_ = ri.element_count();
+        mv_ = p.get_real("max_value", ri.element_type == ElementType::UInt8 ? 255.0 : 1.0);
+        in_ = session().device_array(require_input(), 0);
+        out_ = session().device_array(require_output(), 0);
+    }
+    void record(cudaStream_t s) override {
+        ck(dev::launch_negate(type_, in_, out_, n_, mv_, s), name());
+        mark(s);
+    }
+
+private:
+    int type_ = 0;
+    std::uint64_t n_ = 0;
+    double mv_ = 0;
+    const void* in_ = nullptr;
+    void* out_ = nullptr;
+};
+
+// Shared plan for the two-pass FFT (axis 1 strided, then axis 0 contiguous).
+struct FftPlan {
+    std::uint64_t nx = 0, ny = 0;
+    int dir = 1;
+    bool shift = false;
+    DevMem tw_x, tw_y;
+    dev::LaunchShape s1, s2;
+    void make(std::uint64_t nx_, std::uint64_t ny_, int dir_, std::uint64_t planes, dev::Combine mode,
+              std::uint64_t items, int ordinal) {
+        nx = nx_;
+        ny = ny_;
+        dir = dir_;
+        tw_y = twiddle_table(ny, dir);
+        tw_x = twiddle_table(nx, dir);
+        const int sms = sm_count(ordinal);
+        s1 = dev::plan_strided(ny, nx, planes, sms);
+        s2 = dev::plan_contig(nx, mode, items, sms);
+    }
+};
+
+class Fft2dProcess final : public GraphProcess {
+public:
+    using GraphProcess::GraphProcess;
+    void bake(const ProcessParams& p) override {
+        p.require_known({"direction", "shift", "algorithm"});
+        const std::string d = p.get_string("direction", "forward");
+        if (d != "forward" && d != "inverse")
+            throw InvalidParams(name() + ": direction must be \"forward\" or \"inverse\", got \"" + d + "\"");
+        const std::string algo = p.get_string("algorithm", "stockham");
+        if (algo != "stockham" && algo != "radix2")
+            throw InvalidParams(name() + ": algorithm must be \"stockham\" or \"radix2\"");
+        inverse_ = d == "inverse";
+        shift_ = p.get_bool("shift", false);
+        const LayoutRecord& ri = array_of(input_layout(), 0, name());
+        const LayoutRecord& ro = array_of(output_layout(), 0, name());
+        require_type(ri, ElementType::Complex64, name());
+        if (ro.element_type != ri.element_type || ro.dims != ri.dims)
+            throw ShapeMismatch(name() + ": output " + dims_str(ro) + " does not match input " + dims_str(ri));
+        if (require_input() == require_output())
+            throw InvalidArgument(name() + ": fft2d does not run in place (use distinct input/output data)");
+        nx_ = ri.dims[0];
+        ny_ = ri.rank > 1 ? ri.dims[1] : 1;
+        batch_ = prod(ri, 2, ri.rank);
+        if (!is_pow2(nx_) || !is_pow2(ny_))
+            throw ShapeMismatch(name() + ": spatial dims must be powers of two, got " + dims_str(ri));
+        radix2_ = algo == "radix2" || !dev::fft_size_supported(nx_) || !dev::fft_size_supported(ny_);
+        if (radix2_ && shift_) throw InvalidParams(name() + ": shift requires the stockham algorithm");
+        in_ = static_cast<const float2*>(session().device_array(require_input(), 0));
+        out_ = static_cast<float2*>(session().device_array(require_output(), 0));
+        if (radix2_)
+            bake_radix2();
+        else
+            plan_.make(nx_, ny_, inverse_ ? 1 : -1, batch_, dev::Combine::None, ny_ * batch_,
+                       session().cuda().ordinal());
+    }
+    void record(cudaStream_t s) override {
+        if (radix2_) {
+            record_radix2(s);
+            return;
+        }
+        const float scale = inverse_ ? float(1.0 / (double(nx_) * double(ny_))) : 1.0f;
+        dev::StridedArgs a1{in_, out_, nx_, batch_, shift_, shift_, 1.0f, plan_.tw_y.as<float2>()};
+        ck(dev::launch_strided(ny_, plan_.dir, a1, plan_.s1, s), name() + "/axis1");
+        mark(s);
+        dev::ContigArgs a2{out_, out_, nullptr, ny_, 0, batch_, shift_, shift_, scale, plan_.tw_x.as<float2>()};
+        ck(dev::launch_contig(nx_, plan_.dir, dev::Combine::None, a2, plan_.s2, s), name() + "/axis0");
+        mark(s);
+    }
+
+private:
+    // The reference's own pass sequence on the GPU:
+    // bit-exact with the CPU reference, used for sizes beyond the fused
+    // kernels and on request ("algorithm": "radix2").
+    void bake_radix2() {
+        passes_.clear();
+        const std::uint64_t n = nx_ * ny_ * batch_;
+        const float fs = inverse_ ? float(1.0 / (double(nx_) * double(ny_))) : 1.0f;
+        auto bits = [](std::uint64_t v) { unsigned b = 0; while ((std::uint64_t(1) << b) < v) ++b; return b; };
+        const unsigned bx = bits(nx_), by = bits(ny_);
+        std::vector<std::vector<std::byte>> blocks;
+        for (int axis = 0; axis < 2; ++axis) {
+            const std::uint64_t L = axis == 0 ? nx_ : ny_, S = axis == 0 ? 1 : nx_;
+            const unsigned nb = bits(L);
+            auto header = [&](std::uint32_t mode, std::uint64_t m, float scale, std::size_t payload) {
+                std::vector<std::byte> b(40 + payload);
+                std::memcpy(b.data(), &mode, 4);
+                std::memcpy(b.data() + 8, &L, 8);
+                std::memcpy(b.data() + 16, &S, 8);
+                std::memcpy(b.data() + 24, &m, 8);
+                std::memcpy(b.data() + 32, &scale, 4);
+                return b;
+            };
+            std::vector<std::byte> rb = header(axis == 0 ? 0u : 1u, 0, 1.0f, 4 * L);
+            for (std::uint64_t k = 0; k < L; ++k) {
+                std::uint32_t r = 0;
+                for (unsigned b = 0; b < nb; ++b)
+                    if (k & (std::uint64_t(1) << b)) r |= 1u << (nb - 1 - b);
+                std::memcpy(rb.data() + 40 + 4 * k, &r, 4);
+            }
+            passes_.push_back({blocks.size(), n, axis == 0});
+            blocks.push_back(std::move(rb));
+            for (unsigned pp = 0; pp < nb; ++pp) {
+                const bool last = axis == 0 ? (by == 0 && pp + 1 == bx) : (pp + 1 == by);
+                std::vector<std::byte> tb = header(2u, std::uint64_t(1) << pp, last ? fs : 1.0f, 4 * L);
+                for (std::uint64_t t = 0; t < L / 2; ++t) {
+                    const double th = (inverse_ ? 1.0 : -1.0) * 2.0 * M_PI * double(t) / double(L);
+                    const float c = float(std::cos(th)), sn = float(std::sin(th));
+                    std::memcpy(tb.data() + 40 + 8 * t, &c, 4);
+                    std::memcpy(tb.data() + 44 + 8 * t, &sn, 4);
+                }
+                passes_.push_back({blocks.size(), n / 2, false});
+                blocks.push_back(std::move(tb));
+            }
+        }
+        std::uint64_t total = 0;
+        offsets_.clear();
+        for (auto& b : blocks) {
+            offsets_.push_back(total);
+            total += (b.size() + 255) & ~std::uint64_t(255);
+        }
+        std::vector<std::byte> all(total);
+        for (std::size_t i = 0; i < blocks.size(); ++i) std::memcpy(all.data() + offsets_[i], blocks[i].data(), blocks[i].size());
+        pblock_ = upload_bytes(all.data(), all.size());
+    }
+    void record_radix2(cudaStream_t s) {
+        hetreco_kernel_args a{};
+        a.in = session().device_array(require_input(), 0);
+        a.out = session().device_array(require_output(), 0);
+        // array 0 pointers already include offsets: use a zero-offset header
+        if (!hdr0_.get()) {
+            std::uint64_t h[12] = {1, 0, 4, 1, 1, 1, 1, 1, 1, 1, 1, 1};
+            hdr0_ = upload_bytes(h, sizeof h);
+        }
+        a.in_layout = hdr0_.as<std::uint64_t>();
+        a.out_layout = hdr0_.as<std::uint64_t>();
+        for (const Pass& p : passes_) {
+            hetreco_kernel_args b = a;
+            if (!p.gather) b.in = b.out;
+            b.params = pblock_.as<char>() + offsets_[p.block];
+            ck(dev::launch_builtin(dev::Builtin::FftRadix2Pass, b, p.gsize, s), name() + "/radix2");
+            mark(s);
+        }
+    }
+
+    struct Pass {
+        std::size_t block;
+        std::uint64_t gsize;
+        bool gather;
+    };
+    bool inverse_ = false, shift_ = false, radix2_ = false;
+    std::uint64_t nx_ = 0, ny_ = 0, batch_ = 0;
+    const float2* in_ = nullptr;
+    float2* out_ = nullptr;
+    FftPlan plan_;
+    std::vector<Pass> passes_;
+    std::vector<std::uint64_t> offsets_;
+    DevMem pblock_, hdr0_;
+};
+
+// Wraps one reference-ABI builtin kernel with baked device params.
+class BuiltinProcess final : public GraphProcess {
+public:
+    BuiltinProcess(ComputeSession& s, std::string name, dev::Builtin which)
+        : GraphProcess(s, std::move(name)), which_(which) {}
+    void bake(const ProcessParams& p) override {
+        const LayoutDescriptor& li = input_layout();
+        const LayoutDescriptor& lo = output_layout();
+        const LayoutRecord& x = array_of(li, 0, name());
+        const LayoutRecord& o = array_of(lo, 0, name());
+        std::uint32_t param_word = 0;
+        if (which_ == dev::Builtin::ComplexElementProd) {
+            p.require_known({"conjugate_s"});
+            const LayoutRecord& sm = array_of(li, 1, name());
+            require_type(x, ElementType::Complex64, name());
+            require_type(sm, ElementType::Complex64, name());
+            if (o.element_type != x.element_type || o.dims != x.dims)
+                throw ShapeMismatch(name() + ": output " + dims_str(o) + " does not match x " + dims_str(x));
+            if (x.element_count() % sm.element_count() != 0)
+                throw ShapeMismatch(name() + ": s " + dims_str(sm) + " does not tile x " + dims_str(x));
+            param_word = p.get_bool("conjugate_s", true) ? 1u : 0u;
+            gsize_ = x.element_count();
+        } else {
+            p.require_known({});
+            require_type(x, ElementType::Complex64, name());
+            if (x.rank < 3) throw ShapeMismatch(name() + ": input must be [nx, ny, coils, ...], got " + dims_str(x));
+            const ElementType ot = which_ == dev::Builtin::RssCombine ? ElementType::Float32 : ElementType::Complex64;
+            require_type(o, ot, name());
+            std::vector<std::uint64_t> want{x.dims[0], x.dims[1]};
+            for (std::uint32_t d = 3; d < x.rank; ++d) want.push_back(x.dims[d]);
+            std::uint64_t frames = prod(x, 3, x.rank);
+            const bool ok = o.dims[0] == x.dims[0] && o.dims[1] == x.dims[1] &&
+                            o.element_count() == x.dims[0] * x.dims[1] * frames;
+            if (!ok) throw ShapeMismatch(name() + ": output " + dims_str(o) + " does not match the coil-reduced input");
+            gsize_ = x.dims[0] * x.dims[1] * frames;
+        }
+        params_ = upload_bytes(&param_word, sizeof param_word);
+    }
+    void record(cudaStream_t s) override {
+        hetreco_kernel_args a{};
+        a.in = session().device_array(require_input(), 0);
+        a.out = session().device_array(require_output(), 0);
+        // device_array includes array 0's offset; the headers carry offsets
+        // relative to the buffer base, so pass the base pointers instead.
+        a.in = static_cast<const char*>(a.in) - input_layout().records[0].offset_bytes;
+        a.out = static_cast<char*>(a.out) - output_layout().records[0].offset_bytes;
+        a.in_layout = session().device_header(require_input());
+        a.out_layout = session().device_header(require_output());
+        a.params = params_.get();
+        a.params_size = 4;
+        ck(dev::launch_builtin(which_, a, gsize_, s), name());
+        mark(s);
+    }
+
+private:
+    dev::Builtin which_;
+    std::uint64_t gsize_ = 0;
+    DevMem params_;
+};
+
+// Fused reconstruction: SENSE (Eq. 1) or RSS.
+class ReconProcess final : public GraphProcess {
+public:
+    ReconProcess(ComputeSession& s, std::string name, dev::Combine mode)
+        : GraphProcess(s, std::move(name)), mode_(mode) {}
+    void bake(const ProcessParams& p) override {
+        p.require_known({"shift"});
+        shift_ = p.get_bool("shift", false);
+        const LayoutDescriptor& li = input_layout();
+        const LayoutRecord& y = array_of(li, 0, name());
+        require_type(y, ElementType::Complex64, name());
+        if (y.rank < 3) throw ShapeMismatch(name() + ": k-space must be [nx, ny, coils(, frames)], got " + dims_str(y));
+        nx_ = y.dims[0];
+        ny_ = y.dims[1];
+        nc_ = y.dims[2];
+        nf_ = prod(y, 3, y.rank);
+        if (!is_pow2(nx_) || !is_pow2(ny_) || !dev::fft_size_supported(nx_) || !dev::fft_size_supported(ny_))
+            throw ShapeMismatch(name() + ": spatial dims must be powers of two <= 4096, got " + dims_str(y));
+        const LayoutRecord& o = array_of(output_layout(), 0, name());
+        require_type(o, mode_ == dev::Combine::Sense ? ElementType::Complex64 : ElementType::Float32, name());
+        if (o.dims[0] != nx_ || (o.rank > 1 ? o.dims[1] : 1) != ny_ || o.element_count() != nx_ * ny_ * nf_)
+            throw ShapeMismatch(name() + ": output " + dims_str(o) + " must be [nx, ny, frames] for k-space " + dims_str(y));
+        smap_ = nullptr;
+        if (mode_ == dev::Combine::Sense) {
+            const LayoutRecord& sm = array_of(li, 1, name());
+            require_type(sm, ElementType::Complex64, name());
+            if (sm.dims[0] != nx_ || sm.dims[1] != ny_ || sm.element_count() != nx_ * ny_ * nc_)
+                throw ShapeMismatch(name() + ": sensitivity maps " + dims_str(sm) + " must be [nx, ny, coils]");
+            smap_ = static_cast<const float2*>(session().device_array(require_input(), 1));
+        }
+        y_ = static_cast<const float2*>(session().device_array(require_input(), 0));
+        out_ = session().device_array(require_output(), 0);
+        const std::uint64_t scratch_bytes = nx_ * ny_ * nc_ * nf_ * 8;
+        if (scratch_.size() != scratch_bytes) scratch_ = DevMem(scratch_bytes);
+        plan_.make(nx_, ny_, +1, nc_ * nf_, mode_, ny_ * nf_, session().cuda().ordinal());
+    }
+    void record(cudaStream_t s) override {
+        dev::StridedArgs a1{y_, scratch_.as<float2>(), nx_, nc_ * nf_, shift_, shift_, 1.0f, plan_.tw_y.as<float2>()};
+        ck(dev::launch_strided(ny_, +1, a1, plan_.s1, s), name() + "/axis1");
+        mark(s);
+        dev::ContigArgs a2{scratch_.as<float2>(), out_, smap_, ny_, nc_, nf_, shift_, shift_,
+                           float(1.0 / (double(nx_) * double(ny_))), plan_.tw_x.as<float2>()};
+        ck(dev::launch_contig(nx_, +1, mode_, a2, plan_.s2, s), name() + "/axis0+combine");
+        mark(s);
+    }
+
+private:
+    dev::Combine mode_;
+    bool shift_ = false;
+    std::uint64_t nx_ = 0, ny_ = 0, nc_ = 0, nf_ = 0;
+    const float2* y_ = nullptr;
+    const float2* smap_ = nullptr;
+    void* out_ = nullptr;
+    DevMem scratch_;
+    FftPlan plan_;
+};
+
+}  // namespace
+
+std::unique_ptr<GraphProcess> make_negate(ComputeSession& s, std::string n) {
+    return std::make_unique<NegateProcess>(s, std::move(n));
+}
+std::unique_ptr<GraphProcess> make_fft2d(ComputeSession& s, std::string n) {
+    return std::make_unique<Fft2dProcess>(s, std::move(n));
+}
+std::unique_ptr<GraphProcess> make_complex_element_prod(ComputeSession& s, std::string n) {
+    return std::make_unique<BuiltinProcess>(s, std::move(n), dev::Builtin::ComplexElementProd);
+}
+std::unique_ptr<GraphProcess> make_ximage_sum(ComputeSession& s, std::string n) {
+    return std::make_unique<BuiltinProcess>(s, std::move(n), dev::Builtin::XImageSum);
+}
+std::unique_ptr<GraphProcess> make_rss_combine(ComputeSession& s, std::string n) {
+    return std::make_unique<BuiltinProcess>(s, std::move(n), dev::Builtin::RssCombine);
+}
+std::unique_ptr<GraphProcess> make_sens_recon(ComputeSession& s, std::string n) {
+    return std::make_unique<ReconProcess>(s, std::move(n), dev::Combine::Sense);
+}
+std::unique_ptr<GraphProcess> make_rss_recon(ComputeSession& s, std::string n) {
+    return std::make_unique<ReconProcess>(s, std::move(n), dev::Combine::Rss);
+}
+
+std::unique_ptr<GraphProcess> make_process(ComputeSession& s, std::string_view kind, std::string name) {
+    const std::string n = name.empty() ? std::string(kind) : name;
+    if (kind == "negate") return make_negate(s, n);
+    if (kind == "fft2d") return make_fft2d(s, n);
+    if (kind == "complex_element_prod") return make_complex_element_prod(s, n);
+    if (kind == "ximage_sum") return make_ximage_sum(s, n);
+    if (kind == "rss_combine") return make_rss_combine(s, n);
+    if (kind == "sens_recon") return make_sens_recon(s, n);
+    if (kind == "rss_recon") return make_rss_recon(s, n);
+    throw InvalidArgument("unknown process kind '" + std::string(kind) + "'");
+}
+
+// ---- StreamingRecon ---------------------------------------------------------------------------
+
+struct StreamingRecon::Impl {
+    ComputeSession* session = nullptr;
+    dev::Combine mode = dev::Combine::Sense;
+    bool shift = false;
+    std::uint64_t nx = 0, ny = 0, nc = 0;
+    DevMem smaps, ybuf[2], obuf[2], scratch;
+    FftPlan plan;
+    cudaEvent_t h2d_done[2]{}, y_free[2]{}, comp_done[2]{}, o_free[2]{};
+    ~Impl() {
+        for (int b = 0; b < 2; ++b)
+            for (cudaEvent_t e : {h2d_done[b], y_free[b], comp_done[b], o_free[b]})
+                if (e) cudaEventDestroy(e);
+    }
+};
+
+StreamingRecon::StreamingRecon(ComputeSession& s, Method method, std::uint64_t nx, std::uint64_t ny,
+                               std::uint64_t coils, std::uint64_t chunk, const void* host_smaps, bool shift)
+    : impl_(std::make_unique<Impl>()) {
+    if (!is_pow2(nx) || !is_pow2(ny) || !dev::fft_size_supported(nx) || !dev::fft_size_supported(ny))
+        throw ShapeMismatch("streaming recon: nx, ny must be powers of two <= 4096");
+    if (coils == 0 || chunk == 0) throw InvalidArgument("streaming recon: coils and chunk_frames must be >= 1");
+    Impl& m = *impl_;
+    m.session = &s;
+    m.mode = method == Method::Sense ? dev::Combine::Sense : dev::Combine::Rss;
+    m.shift = shift;
+    m.nx = nx;
+    m.ny = ny;
+    m.nc = coils;
+    chunk_ = chunk;
+    in_frame_bytes_ = nx * ny * coils * 8;
+    out_frame_bytes_ = nx * ny * (method == Method::Sense ? 8 : 4);
+    CudaBackend& cb = s.cuda();
+    cb.make_current();
+    if (method == Method::Sense) {
+        if (!host_smaps) throw InvalidArgument("streaming recon: SENSE needs sensitivity maps");
+        m.smaps = upload_bytes(host_smaps, nx * ny * coils * 8);
+    }
+    for (int b = 0; b < 2; ++b) {
+        m.ybuf[b] = DevMem(in_frame_bytes_ * chunk);
+        m.obuf[b] = DevMem(out_frame_bytes_ * chunk);
+        for (cudaEvent_t* e : {&m.h2d_done[b], &m.y_free[b], &m.comp_done[b], &m.o_free[b]})
+            ck(cudaEventCreateWithFlags(e, cudaEventDisableTiming), "cudaEventCreate");
+    }
+    m.scratch = DevMem(in_frame_bytes_ * chunk);
+    m.plan.make(nx, ny, +1, coils * chunk, m.mode, ny * chunk, cb.ordinal());
+}
+
+StreamingRecon::~StreamingRecon() = default;
+
+void StreamingRecon::run(const void* host_in, std::uint64_t frames, void* host_out) {
+    Impl& m = *impl_;
+    CudaBackend& cb = m.session->cuda();
+    cb.make_current();
+    cudaStream_t cs = cb.compute_stream(), hs = cb.h2d_stream(), ds = cb.d2h_stream();
+    const int sms = sm_count(cb.ordinal());
+    const auto* src = static_cast<const char*>(host_in);
+    auto* dst = static_cast<char*>(host_out);
+    const float scale = float(1.0 / (double(m.nx) * double(m.ny)));
+    // the compute stream may still hold earlier session work
+    ck(cudaEventRecord(m.comp_done[0], cs), "cudaEventRecord");
+    ck(cudaStreamWaitEvent(hs, m.comp_done[0], 0), "cudaStreamWaitEvent");
+    for (std::uint64_t k = 0, f0 = 0; f0 < frames; ++k, f0 += chunk_) {
+        const int b = int(k & 1);
+        const std::uint64_t nf = std::min(chunk_, frames - f0);
+        // H2D of this chunk once the compute pass of chunk k-2 released the slab
+        if (k >= 2) ck(cudaStreamWaitEvent(hs, m.y_free[b], 0), "wait y_free");
+        ck(cudaMemcpyAsync(m.ybuf[b].get(), src + f0 * in_frame_bytes_, nf * in_frame_bytes_, cudaMemcpyHostToDevice, hs),
+           "H2D chunk");
+        ck(cudaEventRecord(m.h2d_done[b], hs), "record h2d_done");
+        // compute
+        ck(cudaStreamWaitEvent(cs, m.h2d_done[b], 0), "wait h2d_done");
+        if (k >= 2) ck(cudaStreamWaitEvent(cs, m.o_free[b], 0), "wait o_free");
+        dev::LaunchShape s1 = m.plan.s1, s2 = m.plan.s2;
+        if (nf != chunk_) {
+            s1 = dev::plan_strided(m.ny, m.nx, m.nc * nf, sms);
+            s2 = dev::plan_contig(m.nx, m.mode, m.ny * nf, sms);
+        }
+        dev::StridedArgs a1{m.ybuf[b].as<float2>(), m.scratch.as<float2>(), m.nx, m.nc * nf, m.shift, m.shift, 1.0f,
+                            m.plan.tw_y.as<float2>()};
+        ck(dev::launch_strided(m.ny, +1, a1, s1, cs), "streaming axis1");
+        ck(cudaEventRecord(m.y_free[b], cs), "record y_free");
+        dev::ContigArgs a2{m.scratch.as<float2>(), m.obuf[b].get(), m.smaps.as<float2>(), m.ny, m.nc, nf,
+                           m.shift, m.shift, scale, m.plan.tw_x.as<float2>()};
+        ck(dev::launch_contig(m.nx, +1, m.mode, a2, s2, cs), "streaming axis0+combine");
+        ck(cudaEventRecord(m.comp_done[b], cs), "record comp_done");
+        // D2H
+        ck(cudaStreamWaitEvent(ds, m.comp_done[b], 0), "wait comp_done");
+        ck(cudaMemcpyAsync(dst + f0 * out_frame_bytes_, m.obuf[b].get(), nf * out_frame_bytes_, cudaMemcpyDeviceToHost, ds),
+           "D2H chunk");
+        ck(cudaEventRecord(m.o_free[b], ds), "record o_free");
+    }
+    const cudaError_t e = cudaStreamSynchronize(ds);
+    if (e != cudaSuccess) throw DeviceError("streaming_recon", cudaGetErrorString(e));
+    ck(cudaStreamSynchronize(cs), "streaming recon (compute)");
+}
+
+}  // namespace hetreco

@@ -1,0 +1,220 @@
+// fft_core.cuh -- register/shared-memory building blocks of the batched FFT.
+//
+// A line of N = 2^n complex samples is owned by T = N/R threads; thread j
+// keeps R samples in registers, slot m <-> position j + T*m.  The transform
+// is a Stockham autosort sequence of radix passes (radix list per N below):
+// in a pass of radix Rp after `Ns` points have been combined, thread j runs
+// R/Rp in-register DFT_Rp's (groups g = j + s*T), each on slots
+// m = s + q*(R/Rp), after multiplying by W_{Ns*Rp}^{(g mod Ns) q}; results go
+// to shared position (g/Ns)*Ns*Rp + g%Ns + q*Ns.  Every pass reads slot m from
+// position j + T*m, so only passes 2.. touch shared memory, and the last
+// pass leaves the output in natural order in the same slots -- first-pass
+// loads and last-pass stores are the coalesced pattern j + T*m.
+//
+// The in-register DFTs are radix-2 DIT with compile-time twiddles; trivial
+// twiddles (1, -1, +-i) cost nothing and the (1 +- i)/sqrt2 ones cost 2 FMUL.
+//
+// This replaces the reference's per-pass, one-butterfly-per-work-item
+// formulation (kernels/fft_radix2_pass.cl.src:22-69), which sweeps the whole
+// array log2(N)+1 times per axis, with one HBM read and one HBM write per axis.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <type_traits>
+#include <utility>
+
+namespace hetreco::dev {
+
+// ---- compile-time helpers ---------------------------------------------------------
+
+template <class F, int... Is>
+__device__ __forceinline__ void sfor_impl(F&& f, std::integer_sequence<int, Is...>) {
+    (f(std::integral_constant<int, Is>{}), ...);
+}
+// Calls f(std::integral_constant<int, i>) for i = 0..N-1 (fully unrolled).
+template <int N, class F>
+__device__ __forceinline__ void sfor(F&& f) {
+    sfor_impl(f, std::make_integer_sequence<int, N>{});
+}
+
+constexpr int ilog2c(int v) { return v <= 1 ? 0 : 1 + ilog2c(v / 2); }
+
+constexpr int bitrev_c(int v, int bits) {
+    int r = 0;
+    for (int b = 0; b < bits; ++b)
+        if (v & (1 << b)) r |= 1 << (bits - 1 - b);
+    return r;
+}
+
+// cos(2 pi k / 64): first quadrant literal values (17 significant digits),
+// the rest by symmetry.
+constexpr double kQuarterCos[17] = {
+    1.0, 0.9951847266721969, 0.9807852804032304, 0.9569403357322088, 0.9238795325112867,
+    0.881921264348355, 0.8314696123025452, 0.773010453362737, 0.7071067811865476,
+    0.6343932841636455, 0.5555702330196023, 0.4713967368259978, 0.38268343236508984,
+    0.29028467725446233, 0.19509032201612833, 0.09801714032956077, 0.0};
+
+constexpr double cos64(int k) {
+    k = ((k % 64) + 64) % 64;
+    return k <= 16 ? kQuarterCos[k]
+         : k <= 32 ? -kQuarterCos[32 - k]
+         : k <= 48 ? -kQuarterCos[k - 32]
+                   : kQuarterCos[64 - k];
+}
+constexpr double sin64(int k) { return cos64(k - 16); }
+
+// ---- complex arithmetic ---------------------------------------------------------------
+
+__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ float2 cmul(float2 a, float2 b) {
+    return make_float2(fmaf(a.x, b.x, -a.y * b.y), fmaf(a.x, b.y, a.y * b.x));
+}
+__device__ __forceinline__ float2 cscale(float2 a, float s) { return make_float2(a.x * s, a.y * s); }
+
+// v * W_N^K with W_N = exp(DIR * 2 pi i / N), N | 64, all at compile time.
+template <int N, int K, int DIR>
+__device__ __forceinline__ float2 wmul(float2 v) {
+    constexpr int k = ((K % N) + N) % N;
+    if constexpr (k == 0) {
+        return v;
+    } else if constexpr (2 * k == N) {
+        return make_float2(-v.x, -v.y);
+    } else if constexpr (4 * k == N) {  // angle DIR*pi/2
+        return DIR > 0 ? make_float2(-v.y, v.x) : make_float2(v.y, -v.x);
+    } else if constexpr (4 * k == 3 * N) {  // angle DIR*3pi/2
+        return DIR > 0 ? make_float2(v.y, -v.x) : make_float2(-v.y, v.x);
+    } else {
+        constexpr int idx = k * (64 / N);
+        constexpr float c = float(cos64(idx));
+        constexpr float s = float(DIR * sin64(idx));
+        if constexpr ((8 * k) % N == 0) {
+            // odd multiple of pi/4: |c| == |s| == sqrt(2)/2
+            constexpr float h = c;  // c = +-h
+            constexpr float r = s / c;  // +-1
+            return make_float2(h * (v.x - r * v.y), h * (v.y + r * v.x));
+        } else {
+            return make_float2(fmaf(c, v.x, -s * v.y), fmaf(c, v.y, s * v.x));
+        }
+    }
+}
+
+// In-register DFT of Rp points stored at v[OFF + q*STR], q = 0..Rp-1, natural
+// order in and out.  Radix-2 decimation in time.
+template <int Rp, int DIR, int STR, int OFF, int R>
+__device__ __forceinline__ void dft_regs(float2 (&v)[R]) {
+    if constexpr (Rp == 1) {
+        return;
+    } else {
+        constexpr int bits = ilog2c(Rp);
+        float2 a[Rp];
+        sfor<Rp>([&](auto i) { a[i.value] = v[OFF + bitrev_c(i.value, bits) * STR]; });
+        sfor<bits>([&](auto st) {
+            constexpr int m = 2 << st.value;  // span of this stage
+            constexpr int h = m / 2;
+            sfor<Rp / m>([&](auto b) {
+                sfor<h>([&](auto kk) {
+                    constexpr int i0 = b.value * m + kk.value;
+                    const float2 t = wmul<m, kk.value, DIR>(a[i0 + h]);
+                    const float2 u = a[i0];
+                    a[i0] = cadd(u, t);
+                    a[i0 + h] = csub(u, t);
+                });
+            });
+        });
+        sfor<Rp>([&](auto i) { v[OFF + i.value * STR] = a[i.value]; });
+    }
+}
+
+// ---- per-size plan ------------------------------------------------------------------------
+
+// Radix lists: first radix == R (points per thread), product == N.
+template <int N> struct Plan;
+template <> struct Plan<1>    { static constexpr int R = 1;  static constexpr int P = 0; static constexpr int rad[1] = {1}; };
+template <> struct Plan<2>    { static constexpr int R = 2;  static constexpr int P = 1; static constexpr int rad[1] = {2}; };
+template <> struct Plan<4>    { static constexpr int R = 4;  static constexpr int P = 1; static constexpr int rad[1] = {4}; };
+template <> struct Plan<8>    { static constexpr int R = 8;  static constexpr int P = 1; static constexpr int rad[1] = {8}; };
+template <> struct Plan<16>   { static constexpr int R = 16; static constexpr int P = 1; static constexpr int rad[1] = {16}; };
+template <> struct Plan<32>   { static constexpr int R = 8;  static constexpr int P = 2; static constexpr int rad[2] = {8, 4}; };
+template <> struct Plan<64>   { static constexpr int R = 8;  static constexpr int P = 2; static constexpr int rad[2] = {8, 8}; };
+template <> struct Plan<128>  { static constexpr int R = 16; static constexpr int P = 2; static constexpr int rad[2] = {16, 8}; };
+template <> struct Plan<256>  { static constexpr int R = 16; static constexpr int P = 2; static constexpr int rad[2] = {16, 16}; };
+template <> struct Plan<512>  { static constexpr int R = 16; static constexpr int P = 3; static constexpr int rad[3] = {16, 16, 2}; };
+template <> struct Plan<1024> { static constexpr int R = 16; static constexpr int P = 3; static constexpr int rad[3] = {16, 16, 4}; };
+template <> struct Plan<2048> { static constexpr int R = 16; static constexpr int P = 3; static constexpr int rad[3] = {16, 16, 8}; };
+template <> struct Plan<4096> { static constexpr int R = 16; static constexpr int P = 3; static constexpr int rad[3] = {16, 16, 16}; };
+
+template <int N>
+struct LineFFT {
+    using PL = Plan<N>;
+    static constexpr int R = PL::R;
+    static constexpr int T = N / R;
+    static constexpr int P = PL::P;
+
+    static constexpr int radix(int p) { return PL::rad[p]; }
+    static constexpr int ns(int p) { return p == 0 ? 1 : ns(p - 1) * radix(p - 1); }
+    // twiddle registers needed by pass p (p >= 1) and their offset
+    static constexpr int tw_count(int p) { return p == 0 ? 0 : (R / radix(p)) * (radix(p) - 1); }
+    static constexpr int tw_offset(int p) { return p <= 1 ? 0 : tw_offset(p - 1) + tw_count(p - 1); }
+    static constexpr int NTW = P == 0 ? 1 : tw_offset(P - 1) + tw_count(P - 1) + 1;
+
+    // Padded shared-memory index: one 8-byte pad per 16 samples.
+    __device__ __forceinline__ static int pad(int p) { return p + (p >> 4); }
+    static constexpr int padded_len = N + (N >> 4);
+
+    // Loads this thread's pass twiddles from the W_N^t table (DIR applied).
+    __device__ __forceinline__ static void load_twiddles(float2 (&tw)[NTW], const float2* __restrict__ table,
+                                                         int j) {
+        sfor<P>([&](auto pc) {
+            constexpr int p = pc.value;
+            if constexpr (p >= 1) {
+                constexpr int Rp = radix(p), Ns = ns(p), S = R / Rp;
+                constexpr int stride = N / (Ns * Rp);
+                sfor<S>([&](auto sc) {
+                    const int g = j + sc.value * T;
+                    const int gm = g % Ns;
+                    sfor<Rp - 1>([&](auto qc) {
+                        constexpr int q = qc.value + 1;
+                        tw[tw_offset(p) + sc.value * (Rp - 1) + qc.value] = __ldg(&table[gm * q * stride]);
+                    });
+                });
+            }
+        });
+    }
+
+    // Runs all passes.  `line` is this line's shared buffer (padded_len
+    // float2), `sync` a callable that synchronises the threads of the line.
+    template <int DIR, class Sync>
+    __device__ __forceinline__ static void run(float2 (&v)[R], const float2 (&tw)[NTW], float2* line, int j,
+                                               Sync&& sync) {
+        sfor<P>([&](auto pc) {
+            constexpr int p = pc.value;
+            constexpr int Rp = radix(p), Ns = ns(p), S = R / Rp;
+            if constexpr (p >= 1) {
+                // exchange: write previous pass' outputs, read this pass' inputs
+                constexpr int Rq = radix(p - 1), Nq = ns(p - 1), Sq = R / Rq;
+                sync();
+                sfor<Sq>([&](auto sc) {
+                    const int g = j + sc.value * T;
+                    const int base = (g / Nq) * Nq * Rq + (g % Nq);
+                    sfor<Rq>([&](auto qc) { line[pad(base + qc.value * Nq)] = v[sc.value + qc.value * Sq]; });
+                });
+                sync();
+                sfor<R>([&](auto m) { v[m.value] = line[pad(j + T * m.value)]; });
+                // twiddles
+                sfor<S>([&](auto sc) {
+                    sfor<Rp - 1>([&](auto qc) {
+                        constexpr int m = sc.value + (qc.value + 1) * S;
+                        v[m] = cmul(v[m], tw[tw_offset(p) + sc.value * (Rp - 1) + qc.value]);
+                    });
+                });
+            }
+            sfor<S>([&](auto sc) { dft_regs<Rp, DIR, S, sc.value>(v); });
+            (void)Ns;
+        });
+    }
+};
+
+}  // namespace hetreco::dev

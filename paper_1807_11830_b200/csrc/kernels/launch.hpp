@@ -1,0 +1,95 @@
+// launch.hpp -- host-side entry points of the sm_100a kernels.
+// Everything here enqueues asynchronously on the given stream and returns the
+// launch status; nothing synchronises.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "hetreco_b200/device_abi.h"
+
+namespace hetreco::dev {
+
+// ---- reference-ABI builtins (kernels/*.cl.src semantics, bit-exact) ---------------
+
+enum class Builtin : int {
+    Negate = 0,
+    FftRadix2Pass,
+    ComplexElementProd,
+    XImageSum,
+    RssCombine,
+    MatrixAdd,
+    Count
+};
+const char* builtin_name(Builtin b);
+int builtin_from_name(const char* name);  // -1 when unknown
+
+// `args` holds device pointers (params too); gsize as in the reference.
+cudaError_t launch_builtin(Builtin which, const hetreco_kernel_args& args, std::uint64_t gsize,
+                           cudaStream_t stream);
+
+// ---- fast paths used by the processes ----------------------------------------------
+
+// out[i] = max - in[i] for n elements of type UINT8 or FLOAT32 (negate.cl.src),
+// vectorised 16 B per thread.
+cudaError_t launch_negate(int type_code, const void* in, void* out, std::uint64_t n, double max_value,
+                          cudaStream_t stream);
+
+// Supported FFT line lengths (powers of two 1..4096).
+bool fft_size_supported(std::uint64_t n);
+
+// Strided-axis pass: transforms every column (stride nx) of the [nx, N, planes]
+// array along axis 1.  `tw` = device table of W_N^t (direction applied).
+struct StridedArgs {
+    const float2* in;
+    float2* out;
+    std::uint64_t nx;
+    std::uint64_t planes;
+    int shift_in;   // ifftshift along the axis on load
+    int shift_out;  // fftshift along the axis on store
+    float scale;
+    const float2* tw;
+};
+
+enum class Combine : int { None = 0, Sense = 1, Rss = 2 };
+
+// Contiguous-axis pass (axis 0, lines of N samples) with an optional coil
+// combine epilogue.
+//   None : `lines` = ny*batch independent lines, out = float2 lines.
+//   Sense: in = [N, ny, C, F] lines, smap = [N, ny, C];
+//          out[x,y,f] = sum_c conj(smap[x,y,c]) * X[x,y,c,f]   (COMPLEX64)
+//   Rss  : out[x,y,f] = sqrt(sum_c |X[x,y,c,f]|^2)            (FLOAT32)
+// The combine multiplies in fp32 with the reference's rounding order and
+// accumulates in fp64 in coil order (complex_element_prod.cl.src,
+// ximage_sum.cl.src, rss_combine.cl.src).
+struct ContigArgs {
+    const float2* in;
+    void* out;
+    const float2* smap;
+    std::uint64_t ny;
+    std::uint64_t coils;   // Sense/Rss only
+    std::uint64_t frames;  // Sense/Rss: F; None: batch
+    int shift_in;
+    int shift_out;
+    float scale;
+    const float2* tw;
+};
+
+struct LaunchShape {
+    int block = 0;
+    int grid = 0;
+    int smem = 0;
+};
+
+// Pick block/grid/smem for a given problem (called once at init, baked into
+// the process' CUDA graph).
+LaunchShape plan_strided(std::uint64_t N, std::uint64_t nx, std::uint64_t planes, int device_sms);
+LaunchShape plan_contig(std::uint64_t N, Combine mode, std::uint64_t items, int device_sms);
+
+cudaError_t launch_strided(std::uint64_t N, int dir, const StridedArgs& a, const LaunchShape& s,
+                           cudaStream_t stream);
+cudaError_t launch_contig(std::uint64_t N, int dir, Combine mode, const ContigArgs& a,
+                          const LaunchShape& s, cudaStream_t stream);
+
+}  // namespace hetreco::dev

@@ -1,0 +1,444 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the oracle.
+
+Bar (BASELINE.json north_star): negate, layout/indexing and the builtin
+reference-ABI kernels are BIT-EXACT with the reference; the fused FFT and the
+recon chains are within max|d|/max|ref| <= 1e-5 (fp32) of the oracle.
+"""
+import struct
+
+import numpy as np
+import pytest
+
+from oracle import oracle as o
+from paper_1807_11830_b200 import hetreco as h
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-5  # max|d| / max|ref|, north_star
+
+
+def relmax(a, ref):
+    ref = np.asarray(ref)
+    return float(np.abs(np.asarray(a) - ref).max() / max(float(np.abs(ref).max()), 1e-30))
+
+
+def beq(a, b):
+    a, b = np.asarray(a), np.asarray(b)
+    return a.shape == b.shape and a.dtype == b.dtype and a.tobytes(order="F") == b.tobytes(order="F")
+
+
+def cplx(rng, *shape):
+    return np.asfortranarray((rng.standard_normal(shape) + 1j * rng.standard_normal(shape)).astype(np.complex64))
+
+
+@pytest.fixture(scope="module")
+def s():
+    sess = h.ComputeSession("gpu")
+    sess.load_builtin_kernels()
+    yield sess
+    sess.close()
+
+
+def run_process(s, kind, inputs, out_shapes, params=None, kind_in=h.DataKind.KData):
+    hin = s.register_data(h.Data(inputs, kind_in))
+    hout = s.allocate_data(out_shapes, h.DataKind.XData)
+    p = h.Process(s, kind).set_input(hin).set_output(hout).init(params or {})
+    p.launch()
+    res = s.fetch_data(hout).arrays
+    s.release_data(hin)
+    s.release_data(hout)
+    return res, p
+
+
+# ---- device, session plumbing -------------------------------------------------------------
+
+def test_device_is_b200_class(s):
+    d = s.device()
+    assert d.device_type == h.DeviceType.Gpu and d.vendor == "NVIDIA"
+    assert d.api_version.startswith("10."), d.api_version  # sm_100
+    assert d.base_alignment_bytes == 256
+
+
+def test_register_fetch_roundtrip_and_counters(s):
+    rng = np.random.default_rng(1)
+    arrays = [rng.integers(0, 255, (7, 3), dtype=np.uint8), rng.standard_normal((5,)).astype(np.float64),
+              cplx(rng, 4, 4, 2), np.arange(11, dtype=np.int32)]
+    s.reset_counters()
+    hd = s.register_data(h.Data(arrays, h.DataKind.Generic))
+    back = s.fetch_data(hd).arrays
+    for a, b in zip(arrays, back):
+        assert beq(a, b)
+    assert s.counters() == {"host_to_device": 1, "device_to_host": 1}
+    _, words = h.pack_layout(arrays)
+    assert s.fetch_header_bytes(hd) == words.tobytes()
+    s.release_data(hd)
+    with pytest.raises(h.UnknownHandle):
+        s.fetch_data(hd)
+    with pytest.raises(h.UnknownHandle):
+        s.release_data(hd)
+
+
+def test_copy_array_and_shape_checks(s):
+    a = np.arange(12, dtype=np.float32).reshape(3, 4, order="F")
+    h1 = s.register_data([a, np.zeros(3, np.float32)])
+    h2 = s.register_data([np.zeros(2, np.int32), np.zeros((3, 4), np.float32)])
+    s.copy_array(h1, 0, h2, 1)
+    assert beq(s.fetch_data(h2).arrays[1], a)
+    with pytest.raises(h.ShapeMismatch):
+        s.copy_array(h1, 1, h2, 1)
+    with pytest.raises(h.InvalidArgument):
+        s.copy_array(h1, 5, h2, 1)
+
+
+def test_foreign_handle_rejected(s):
+    other = h.ComputeSession("gpu")
+    hd = other.register_data([np.zeros(4, np.float32)])
+    with pytest.raises(h.UnknownHandle):
+        s.fetch_data(hd)
+    other.close()
+
+
+def test_backend_capacity_and_ranges():
+    b = h.CudaBackend(0, capacity_bytes=1 << 20)
+    buf = b.allocate(1 << 19)
+    with pytest.raises(h.AllocationFailure):
+        b.allocate(1 << 20)
+    with pytest.raises(h.InvalidArgument):
+        b.upload(buf, (1 << 19) - 4, b"12345678")
+    b.upload(buf, 8, b"abcd")
+    assert b.download(buf, 0, 16) == b"\0" * 8 + b"abcd" + b"\0" * 4
+    b.release(buf)
+    with pytest.raises(h.UnknownHandle):
+        b.release(buf)
+    b.close()
+
+
+def test_builtin_registry(s):
+    assert set(s.kernel_names()) == {"negate", "fft_radix2_pass", "complex_element_prod", "ximage_sum",
+                                     "rss_combine", "matrix_add"}
+    with pytest.raises(h.UnsupportedSource):
+        s.load_kernels([("broken.cl.src", "this is not a kernel")])
+    hd = s.register_data([np.zeros(4, np.float32)])
+    with pytest.raises(h.UnknownKernel):
+        s.launch_kernel("nonexistent", hd, hd, b"", 4)
+    with pytest.raises(h.InvalidArgument):
+        s.launch_kernel("negate", hd, hd, struct.pack("<d", 1.0), 0)
+
+
+# ---- reference-ABI kernels: bit-exact with the golden vectors ------------------------------------
+
+def launch_one(s, name, inputs, out_like, params, gsize, in_place=False):
+    hin = s.register_data(inputs)
+    hout = hin if in_place else s.register_data([np.zeros_like(out_like)])
+    s.launch_kernel(name, hin, hout, params, gsize)
+    return s.fetch_data(hout).arrays[0]
+
+
+def test_negate_kernel_bitexact(s, golden):
+    x = golden["negate_u8_in"]
+    for mv in (255.0, 200.0, 300.5, -3.0):
+        got = launch_one(s, "negate", [x], x, struct.pack("<d", mv), x.size)
+        assert beq(got, golden[f"negate_u8_out_{mv}"])
+    f = golden["negate_f32_in"]
+    assert beq(launch_one(s, "negate", [f], f, struct.pack("<d", 1.0), f.size), golden["negate_f32_out"])
+
+
+def test_fft_radix2_pass_kernel_bitexact(s, golden):
+    x = golden["pass_in"]
+    rev = np.array([0, 4, 2, 6, 1, 5, 3, 7], np.uint32)
+    p0 = struct.pack("<IIQQQfI", 0, 0, 8, 1, 0, 1.0, 0) + rev.tobytes()
+    assert beq(launch_one(s, "fft_radix2_pass", [x], x, p0, x.size), golden["pass_mode0"])
+    rev4 = np.array([0, 2, 1, 3], np.uint32)
+    p1 = struct.pack("<IIQQQfI", 1, 0, 4, 8, 0, 1.0, 0) + rev4.tobytes()
+    assert beq(launch_one(s, "fft_radix2_pass", [x], x, p1, x.size, in_place=True), golden["pass_mode1"])
+    tw = np.array([1, 0, 0.70710677, -0.70710677, 0, -1, -0.70710677, -0.70710677], np.float32)
+    p2 = struct.pack("<IIQQQfI", 2, 0, 8, 1, 2, 0.5, 0) + tw.tobytes()
+    assert beq(launch_one(s, "fft_radix2_pass", [x], x, p2, x.size // 2, in_place=True), golden["pass_mode2"])
+
+
+def test_combine_kernels_bitexact(s, golden):
+    x, sm = golden["cep_x"], golden["cep_s"]
+    assert beq(launch_one(s, "complex_element_prod", [x, sm], x, struct.pack("<I", 1), x.size), golden["cep_conj"])
+    assert beq(launch_one(s, "complex_element_prod", [x, sm], x, struct.pack("<I", 0), x.size),
+               golden["cep_noconj"])
+    assert beq(launch_one(s, "ximage_sum", [x], golden["xsum_out"], b"", 16 * 8 * 3), golden["xsum_out"])
+    assert beq(launch_one(s, "rss_combine", [x], golden["rss_out"], b"", 16 * 8 * 3), golden["rss_out"])
+
+
+def test_matrix_add_kernel(s):
+    rng = np.random.default_rng(2)
+    a = rng.standard_normal(1000).astype(np.float32)
+    b = rng.standard_normal(1000).astype(np.float32)
+    assert beq(launch_one(s, "matrix_add", [a, b], a, b"", a.size), o.matrix_add(a, b))
+
+
+# ---- processes ------------------------------------------------------------------------------------
+
+def test_negate_process_bitexact_c1(s):
+    rng = np.random.default_rng(1)
+    x = np.asfortranarray(rng.random((512, 512), dtype=np.float32))
+    (got,), p = run_process(s, "negate", [x], [((512, 512), np.float32)], {"max_value": 1.0})
+    assert beq(got, o.negate(x, 1.0))
+    u = np.asfortranarray(rng.integers(0, 256, (512, 509), dtype=np.uint8))  # ragged tail
+    (got,), _ = run_process(s, "negate", [u], [((512, 509), np.uint8)])
+    assert beq(got, o.negate(u, 255.0))
+    (got,), _ = run_process(s, "negate", [u], [((512, 509), np.uint8)], {"max_value": 100.0})
+    assert beq(got, o.negate(u, 100.0))
+
+
+def test_negate_in_place_and_involution(s):
+    x = np.array([0, 100, 255], np.uint8)
+    hd = s.register_data([x])
+    p = h.Process(s, "negate").set_input(hd).set_output(hd).init()
+    p.launch()
+    assert s.fetch_data(hd).arrays[0].tolist() == [255, 155, 0]
+    p.launch()
+    assert s.fetch_data(hd).arrays[0].tolist() == [0, 100, 255]
+
+
+FFT_SHAPES = [(4, 4, 1), (16, 8, 3), (2, 64, 1), (256, 1, 1), (1, 32, 2), (32, 32, 2), (64, 128, 2),
+              (128, 256, 1), (256, 256, 4), (512, 512, 2), (1024, 64, 1), (8, 2048, 1), (4096, 4, 1)]
+
+
+@pytest.mark.parametrize("shape", FFT_SHAPES, ids=lambda t: "x".join(map(str, t)))
+@pytest.mark.parametrize("direction", ["inverse", "forward"])
+def test_fft2d_process_vs_oracle(s, shape, direction):
+    rng = np.random.default_rng(sum(shape))
+    x = cplx(rng, *shape)
+    (got,), _ = run_process(s, "fft2d", [x], [(shape, np.complex64)], {"direction": direction})
+    ref = o.fft2d(x, direction == "inverse")
+    assert relmax(got, ref) <= TOL
+
+
+@pytest.mark.parametrize("shape", [(16, 8, 3), (64, 32, 1), (256, 256, 1)])
+def test_fft2d_radix2_algorithm_is_bitexact(s, shape):
+    rng = np.random.default_rng(4)
+    x = cplx(rng, *shape)
+    for inverse in (True, False):
+        (got,), _ = run_process(s, "fft2d", [x], [(shape, np.complex64)],
+                                {"direction": "inverse" if inverse else "forward", "algorithm": "radix2"})
+        assert beq(got, o.fft2d(x, inverse))
+
+
+def test_fft2d_golden(s, golden):
+    for name in ("fft_16x8x3", "fft_4x4", "fft_32x32x2", "fft_2x64", "fft_256x1"):
+        x = golden[name + "_in"]
+        (got,), _ = run_process(s, "fft2d", [x], [(x.shape, np.complex64)], {"direction": "inverse"})
+        assert relmax(got, golden[name + "_inv"]) <= TOL
+
+
+def test_fft2d_shift_is_exact_permutation(s):
+    rng = np.random.default_rng(9)
+    x = cplx(rng, 64, 32, 3)
+    (plain,), _ = run_process(s, "fft2d", [x], [(x.shape, np.complex64)], {"direction": "inverse"})
+    xs = np.asfortranarray(np.fft.ifftshift(x, axes=(0, 1)))
+    (ref_shifted_in,), _ = run_process(s, "fft2d", [xs], [(x.shape, np.complex64)], {"direction": "inverse"})
+    (got,), _ = run_process(s, "fft2d", [x], [(x.shape, np.complex64)], {"direction": "inverse", "shift": True})
+    assert beq(got, np.asfortranarray(np.fft.fftshift(ref_shifted_in, axes=(0, 1))))
+    ref = np.fft.fftshift(o.fft2d(np.asfortranarray(np.fft.ifftshift(x, axes=(0, 1))), True), axes=(0, 1))
+    assert relmax(got, ref) <= TOL
+    del plain
+
+
+def test_fft2d_rejects_bad_shapes_and_params(s):
+    x = np.zeros((160, 160), np.complex64)
+    hin = s.register_data([x])
+    hout = s.allocate_data([((160, 160), np.complex64)])
+    with pytest.raises(h.ShapeMismatch):
+        h.Process(s, "fft2d").set_input(hin).set_output(hout).init()
+    y = s.register_data([np.zeros((16, 16), np.complex64)])
+    z = s.allocate_data([((16, 8), np.complex64)])
+    with pytest.raises(h.ShapeMismatch):
+        h.Process(s, "fft2d").set_input(y).set_output(z).init()
+    w = s.allocate_data([((16, 16), np.complex64)])
+    with pytest.raises(h.InvalidParams):
+        h.Process(s, "fft2d").set_input(y).set_output(w).init({"direction": "sideways"})
+    with pytest.raises(h.InvalidParams):
+        h.Process(s, "fft2d").set_input(y).set_output(w).init({"dirction": "inverse"})
+    with pytest.raises(h.UnsupportedElementType):
+        f = s.register_data([np.zeros((16, 16), np.float32)])
+        h.Process(s, "fft2d").set_input(f).set_output(w).init()
+
+
+def test_process_lifecycle(s):
+    x = cplx(np.random.default_rng(0), 32, 32)
+    hin = s.register_data([x])
+    hout = s.allocate_data([((32, 32), np.complex64)])
+    p = h.Process(s, "fft2d").set_input(hin).set_output(hout)
+    with pytest.raises(h.NotInitialized):
+        p.launch()
+    p.init({"direction": "inverse"})
+    with pytest.raises(h.AlreadyInitialized):
+        p.init()
+    s.reset_counters()
+    for _ in range(100):
+        p.launch()
+    st = p.stats()
+    assert st.init_calls == 1 and st.launches == 100
+    assert st.total_launch_seconds > 0 and st.init_seconds > 0
+    assert s.counters() == {"host_to_device": 0, "device_to_host": 0}
+    assert relmax(s.fetch_data(hout).arrays[0], o.fft2d(x, True)) <= TOL
+    # re-point the input between launches (SPEC process: re-point -> new handle consumed)
+    x2 = cplx(np.random.default_rng(1), 32, 32)
+    hin2 = s.register_data([x2])
+    p.set_input(hin2)
+    p.launch()
+    assert relmax(s.fetch_data(hout).arrays[0], o.fft2d(x2, True)) <= TOL
+
+
+@pytest.mark.parametrize("dims", [(16, 8, 4, 3), (32, 16, 1, 2), (64, 64, 8, 1), (256, 256, 8, 1),
+                                  (128, 64, 3, 5), (4, 4, 2, 2), (512, 512, 4, 1), (256, 256, 32, 2)],
+                         ids=lambda t: "x".join(map(str, t)))
+def test_sens_recon_vs_oracle(s, dims):
+    nx, ny, nc, nf = dims
+    rng = np.random.default_rng(nx + nc)
+    Y = cplx(rng, nx, ny, nc, nf)
+    S = cplx(rng, nx, ny, nc)
+    (M,), _ = run_process(s, "sens_recon", [Y, S], [((nx, ny, nf), np.complex64)])
+    assert relmax(M, o.sens_recon(Y, S)) <= TOL
+
+
+@pytest.mark.parametrize("dims", [(16, 8, 4, 3), (256, 256, 8, 1), (128, 32, 1, 4), (512, 512, 4, 1)],
+                         ids=lambda t: "x".join(map(str, t)))
+def test_rss_recon_vs_oracle(s, dims):
+    nx, ny, nc, nf = dims
+    rng = np.random.default_rng(nx * 3 + nc)
+    Y = cplx(rng, nx, ny, nc, nf)
+    (R,), _ = run_process(s, "rss_recon", [Y], [((nx, ny, nf), np.float32)])
+    ref = o.rss_recon(Y)
+    assert relmax(R, ref) <= TOL
+    assert (R >= 0).all()
+
+
+def test_recon_golden(s, golden):
+    Y, S = golden["sens_Y"], golden["sens_S"]
+    (M,), _ = run_process(s, "sens_recon", [Y, S], [((32, 16, 3), np.complex64)])
+    assert relmax(M, golden["sens_M"]) <= TOL
+    (R,), _ = run_process(s, "rss_recon", [golden["rss_Y"]], [((32, 16, 3), np.float32)])
+    assert relmax(R, golden["rss_R"]) <= TOL
+
+
+def test_spec_recon_examples(s):
+    # N=1, S=1 -> M = IFFT(Y); Y=0 -> M=0; 3-4-5 RSS pixel
+    rng = np.random.default_rng(8)
+    Y = cplx(rng, 16, 16, 1, 2)
+    S = np.ones((16, 16, 1), np.complex64)
+    (M,), _ = run_process(s, "sens_recon", [Y, S], [((16, 16, 2), np.complex64)])
+    assert relmax(M, o.fft2d(Y[:, :, 0, :], True)) <= TOL
+    Z = np.zeros((16, 16, 2, 1), np.complex64)
+    (M0,), _ = run_process(s, "sens_recon", [Z, np.ones((16, 16, 2), np.complex64)], [((16, 16, 1), np.complex64)])
+    assert not M0.any()
+    img = np.zeros((8, 8, 2, 1), np.complex64)
+    img[3, 5, 0, 0], img[3, 5, 1, 0] = 3.0, 4.0j
+    Yk = np.asfortranarray(np.fft.fft2(img, axes=(0, 1)).astype(np.complex64))
+    (R,), _ = run_process(s, "rss_recon", [Yk], [((8, 8, 1), np.float32)])
+    assert abs(R[3, 5, 0] - 5.0) <= 1e-5
+
+
+def test_sense_forward_model_roundtrip(s):
+    # SPEC.md:430 / acceptance 1: recovers M_true within rel-L2 1e-4
+    rng = np.random.default_rng(12)
+    nx, ny, nc, nf = 128, 128, 8, 16
+    G = cplx(rng, nx, ny, nc)
+    S = np.asfortranarray((G / np.sqrt((np.abs(G) ** 2).sum(axis=2, keepdims=True))).astype(np.complex64))
+    M = cplx(rng, nx, ny, nf)
+    Y = np.asfortranarray(np.fft.fft2(S[..., None] * M[:, :, None, :], axes=(0, 1)).astype(np.complex64))
+    (rec,), _ = run_process(s, "sens_recon", [Y, S], [((nx, ny, nf), np.complex64)])
+    assert np.linalg.norm(rec - M) / np.linalg.norm(M) <= 1e-4
+
+
+def test_sens_recon_shift(s):
+    rng = np.random.default_rng(21)
+    Y = cplx(rng, 64, 32, 4, 2)
+    S = cplx(rng, 64, 32, 4)
+    (M,), _ = run_process(s, "sens_recon", [Y, S], [((64, 32, 2), np.complex64)], {"shift": True})
+    X = np.fft.fftshift(o.fft2d(np.asfortranarray(np.fft.ifftshift(Y, axes=(0, 1))), True), axes=(0, 1))
+    ref = o.ximage_sum(o.complex_element_prod(np.asfortranarray(X), S, True))
+    assert relmax(M, ref) <= TOL
+
+
+def test_chain_matches_fused_and_oracle(s):
+    # chain(fft2d INVERSE, complex_element_prod conj, ximage_sum) == SimpleMRIRecon
+    rng = np.random.default_rng(5)
+    nx, ny, nc, nf = 64, 32, 4, 3
+    Y = cplx(rng, nx, ny, nc, nf)
+    S = cplx(rng, nx, ny, nc)
+    hk = s.register_data(h.Data([Y], h.DataKind.KData))
+    hx = s.register_data(h.Data([np.zeros_like(Y), S], h.DataKind.XData))
+    hp = s.allocate_data([((nx, ny, nc, nf), np.complex64)], h.DataKind.XData)
+    hm = s.allocate_data([((nx, ny, nf), np.complex64)], h.DataKind.XData)
+    f = h.Process(s, "fft2d").set_input(hk).set_output(hx)
+    c = h.Process(s, "complex_element_prod").set_input(hx).set_output(hp)
+    x = h.Process(s, "ximage_sum").set_input(hp).set_output(hm)
+    f.init({"direction": "inverse"})
+    c.init({"conjugate_s": True})
+    comp = h.chain(s, "simple_mri_recon", [f, c, x])
+    comp.init()
+    s.reset_counters()
+    for _ in range(3):
+        comp.launch()
+    assert s.counters() == {"host_to_device": 0, "device_to_host": 0}  # zero-copy chaining
+    M = s.fetch_data(hm).arrays[0]
+    assert s.counters() == {"host_to_device": 0, "device_to_host": 1}
+    assert relmax(M, o.sens_recon(Y, S)) <= TOL
+    assert comp.stats().launches == 3
+
+
+def test_chain_mismatch(s):
+    a = s.register_data([np.zeros((8, 8), np.complex64)])
+    b = s.allocate_data([((8, 8), np.complex64)])
+    c = s.allocate_data([((8, 8), np.complex64)])
+    p1 = h.Process(s, "fft2d").set_input(a).set_output(b)
+    p2 = h.Process(s, "fft2d").set_input(c).set_output(a)
+    with pytest.raises(h.ChainMismatch):
+        h.chain(s, "bad", [p1, p2])
+
+
+def test_chain_stage_error_carries_index(s):
+    a = s.register_data([np.zeros((8, 8), np.complex64)])
+    b = s.allocate_data([((8, 8), np.complex64)])
+    c = s.allocate_data([((8, 4), np.complex64)])
+    p1 = h.Process(s, "fft2d").set_input(a).set_output(b)
+    p2 = h.Process(s, "fft2d").set_input(b).set_output(c)
+    comp = h.chain(s, "bad", [p1, p2])
+    with pytest.raises(h.ChainStageError) as e:
+        comp.init()
+    assert "stage 1" in str(e.value)
+
+
+def test_streaming_matches_process(s):
+    rng = np.random.default_rng(17)
+    nx, ny, nc, nf = 128, 128, 8, 10
+    Y = h.pinned_empty((nx, ny, nc, nf), np.complex64)
+    Y[...] = cplx(rng, nx, ny, nc, nf)
+    S = cplx(rng, nx, ny, nc)
+    out = h.pinned_empty((nx, ny, nf), np.complex64)
+    st = h.StreamingRecon(s, "sense", nx, ny, nc, 3, S)  # ragged last chunk (10 = 3+3+3+1)
+    st.run(Y, out)
+    assert relmax(out, o.sens_recon(np.asarray(Y), S)) <= TOL
+    outr = h.pinned_empty((nx, ny, nf), np.float32)
+    h.StreamingRecon(s, "rss", nx, ny, nc, 4).run(Y, outr)
+    assert relmax(outr, o.rss_recon(np.asarray(Y))) <= TOL
+
+
+def test_c3_full_size_properties(s):
+    """Full BASELINE C3 size (256^2 x 32 coils x 30 frames): oracle parity on
+    frames sampled from the same launch, plus linearity."""
+    rng = np.random.default_rng(30)
+    nx, ny, nc, nf = 256, 256, 32, 30
+    Y = cplx(rng, nx, ny, nc, nf)
+    S = cplx(rng, nx, ny, nc)
+    hin = s.register_data(h.Data([Y, S], h.DataKind.KData))
+    hout = s.allocate_data([((nx, ny, nf), np.complex64)], h.DataKind.XData)
+    p = h.Process(s, "sens_recon").set_input(hin).set_output(hout).init()
+    p.launch()
+    M = s.fetch_data(hout).arrays[0]
+    for f in (0, 17, 29):
+        ref = o.sens_recon(np.asfortranarray(Y[..., f:f + 1]), S)
+        assert relmax(M[..., f:f + 1], ref) <= TOL
+    # linearity: recon(2.5 Y) == 2.5 recon(Y)
+    h2 = s.register_data(h.Data([np.asfortranarray(Y * np.float32(2.5)), S], h.DataKind.KData))
+    p.set_input(h2)
+    p.launch()
+    M2 = s.fetch_data(hout).arrays[0]
+    assert relmax(M2, 2.5 * M) <= TOL
