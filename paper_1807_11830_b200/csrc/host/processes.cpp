@@ -301,6 +301,7 @@ void GraphProcess::capture() {
         cudaStreamEndCapture(cs, &g);
         if (g) cudaGraphDestroy(g);
         cudaStreamDestroy(cs);
+        cudaGetLastError();  // an invalidated capture must not poison later calls
         throw;
     }
     const cudaError_t e = cudaStreamEndCapture(cs, &g);
@@ -589,16 +590,15 @@ private:
         std::vector<std::byte> all(total);
         for (std::size_t i = 0; i < blocks.size(); ++i) std::memcpy(all.data() + offsets_[i], blocks[i].data(), blocks[i].size());
         pblock_ = upload_bytes(all.data(), all.size());
+        // array pointers passed to the kernel already include the offsets
+        const std::uint64_t h[12] = {1, 0, 4, 1, 1, 1, 1, 1, 1, 1, 1, 1};
+        hdr0_ = upload_bytes(h, sizeof h);
     }
     void record_radix2(cudaStream_t s) {
         hetreco_kernel_args a{};
         a.in = session().device_array(require_input(), 0);
         a.out = session().device_array(require_output(), 0);
         // array 0 pointers already include offsets: use a zero-offset header
-        if (!hdr0_.get()) {
-            std::uint64_t h[12] = {1, 0, 4, 1, 1, 1, 1, 1, 1, 1, 1, 1};
-            hdr0_ = upload_bytes(h, sizeof h);
-        }
         a.in_layout = hdr0_.as<std::uint64_t>();
         a.out_layout = hdr0_.as<std::uint64_t>();
         for (const Pass& p : passes_) {

@@ -80,6 +80,7 @@ struct LaunchShape {
     int block = 0;
     int grid = 0;
     int smem = 0;
+    int variant = 0;  // combine kernel variant (fp32 acc / register prefetch)
 };
 
 // Pick block/grid/smem for a given problem (called once at init, baked into
