@@ -161,6 +161,11 @@ def cpu_baseline(Y, S, budget_s: float = 12.0):
 
 
 def run_reference(args):
+    """The reference's own CPU implementation (oracle/_ref: the unmodified
+    reference library driven through its ComputeSession API).  One step =
+    register the k-space of a bounded frame sample (the reference's H2D),
+    run the SENSE chain, fetch the images (D2H); sensitivity maps and the FFT
+    plan are set up once, as on the B200 arm."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
@@ -168,23 +173,28 @@ def run_reference(args):
     Y, S = make_inputs(1234)
     sample = 2
     Ys = np.asfortranarray(Y[..., :sample])
-    kind = "reference" if o.reference_available() else "port"
-    fn = (lambda: o.ref_recon("sens", Ys, S, reps=1)) if kind == "reference" else (lambda: o.sens_recon(Ys, S))
-    for _ in range(max(1, min(args.warmup, 3))):
-        fn()
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        fn()
-    dt = time.perf_counter() - t0
-    value = sample * args.steps / dt
-    cores = o.ref_pool_threads() if kind == "reference" else 1
+    if o.reference_available():
+        kind = "reference"
+        o.ref_recon_e2e("sens", Ys, S, reps=max(1, min(args.warmup, 2)))
+        _, mean_s = o.ref_recon_e2e("sens", Ys, S, reps=args.steps)
+        cores = o.ref_pool_threads()
+    else:
+        kind = "port"
+        o.sens_recon(Ys, S)
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            o.sens_recon(Ys, S)
+        mean_s = (time.perf_counter() - t0) / args.steps
+        cores = 1
+    value = sample / mean_s
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True,
+            "warmup": args.warmup, "ms_per_step": mean_s * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded N(0,1) k-space)",
             "config": dict(CONFIG, sample_frames_per_step=sample), "impl": "reference",
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind,
-                             "sample": f"{sample} of 30 C3 frames per step through the reference "
-                                       f"ComputeSession (fft_radix2_pass x18 + complex_element_prod + ximage_sum)"},
+                             "sample": f"{sample} of 30 C3 frames per step: register_data(k-space) + "
+                                       f"fft_radix2_pass x18 + complex_element_prod + ximage_sum + fetch_data; "
+                                       f"WorkerPool threads = min(hw,16) of {os.cpu_count()} host cores"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -223,14 +233,15 @@ def run_ours(args):
     clocks = sampler.summary()
 
     # per-kernel device times (events between kernels on the compute stream)
-    k_axis1, k_axis0 = p.profile(reps=10)
+    prof = p.profile(reps=10)  # [axis1, combine] per frame chunk (one chunk by default)
+    k_axis1, k_axis0 = sum(prof[0::2]), sum(prof[1::2])
     bytes_axis1 = 2 * FRAME_Y * NF                 # read Y, write X
     bytes_axis0 = FRAME_Y * NF + SMAP + FRAME_M * NF  # read X + S, write M
     peak, peak_kind = peaks()
     kernels = [
-        {"name": "k_fft_strided<256> (axis-1 IFFT)", "seconds": k_axis1, "bytes": bytes_axis1,
+        {"name": "k_fft_strided<256,+1,256,16> (axis-1 IFFT, column tiles)", "seconds": k_axis1, "bytes": bytes_axis1,
          "gbs": bytes_axis1 / k_axis1 / 1e9},
-        {"name": "k_fft_contig<256,SENSE> (axis-0 IFFT + conj(S) combine)", "seconds": k_axis0,
+        {"name": "k_fft_combine<256,SENSE,fp32,prefetch> (axis-0 IFFT + conj(S) coil combine)", "seconds": k_axis0,
          "bytes": bytes_axis0, "gbs": bytes_axis0 / k_axis0 / 1e9},
     ]
     for k in kernels:

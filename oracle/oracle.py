@@ -97,6 +97,8 @@ def reference():
             lib.refdrv_fft2d.argtypes = [_vp, _vp, _u64, _u64, _u64, _i32]
             lib.refdrv_recon.argtypes = [_i32, _vp, _vp, _vp, _u64, _u64, _u64, _u64, _i32,
                                          C.POINTER(_f64), C.POINTER(_f64)]
+            lib.refdrv_recon_e2e.argtypes = [_i32, _vp, _vp, _vp, _u64, _u64, _u64, _u64, _i32,
+                                             C.POINTER(_f64)]
             lib.refdrv_layout_header.argtypes = [_i32, _vp, _vp, _vp, _u64, _vp, C.POINTER(_u64)]
             _ref = lib
         return _ref
@@ -261,6 +263,23 @@ def ref_recon(method: str, Y: np.ndarray, S: np.ndarray | None = None, reps: int
                                         _p(S) if S is not None else None, _p(out), nx, ny, nc,
                                         nf, reps, C.byref(mean_s), C.byref(init_s)))
     return out, mean_s.value, init_s.value
+
+
+def ref_recon_e2e(method: str, Y: np.ndarray, S: np.ndarray | None = None, reps: int = 1):
+    """Per-step register(Y) + chain + fetch through the reference API.
+    Returns (result, mean_seconds_per_step)."""
+    Y = _f(Y, np.complex64)
+    nx, ny, nc, nf = (Y.shape + (1,))[:4]
+    if method == "sens":
+        S = _f(S, np.complex64)
+        out = np.empty((nx, ny, nf), np.complex64, order="F")
+    else:
+        out = np.empty((nx, ny, nf), np.float32, order="F")
+    mean_s = C.c_double()
+    _check_ref(reference().refdrv_recon_e2e(0 if method == "sens" else 1, _p(Y),
+                                            _p(S) if S is not None else None, _p(out), nx, ny, nc, nf,
+                                            reps, C.byref(mean_s)))
+    return out, mean_s.value
 
 
 def ref_pool_threads() -> int:

@@ -242,6 +242,62 @@ int refdrv_recon(int method, const float* Y, const float* S, void* out, uint64_t
     });
 }
 
+// End-to-end per step through the reference API, the CPU analogue of the
+// B200 e2e measurement: S and the plan are set up once (excluded, like the
+// B200 arm's init), then every step registers the k-space (the reference's
+// "send the data to the computing device", session.cpp:60-83), runs the
+// chain, fetches the images (session.cpp:85-98) and releases the k-space.
+// Writes the last result to `out`, mean seconds per step to *mean_s.
+int refdrv_recon_e2e(int method, const float* Y, const float* S, void* out, uint64_t nx, uint64_t ny,
+                     uint64_t C, uint64_t F, int reps, double* mean_s) {
+    return guarded([&] {
+        ComputeSession s(*backend());
+        s.load_builtin_kernels();
+        std::vector<NDArray> ax;
+        ax.push_back(c64({nx, ny, C, F}, nullptr));
+        if (method == 0) ax.push_back(c64({nx, ny, C}, S));
+        DataHandle hx = s.register_data(Data(std::move(ax), DataKind::XData));
+        DataHandle hp{}, hm{};
+        if (method == 0) {
+            std::vector<NDArray> ap;
+            ap.push_back(c64({nx, ny, C, F}, nullptr));
+            hp = s.register_data(Data(std::move(ap), DataKind::XData));
+            std::vector<NDArray> am;
+            am.push_back(c64({nx, ny, F}, nullptr));
+            hm = s.register_data(Data(std::move(am), DataKind::XData));
+        } else {
+            std::vector<NDArray> am;
+            am.push_back(NDArray(ElementType::Float32, {nx, ny, F}));
+            hm = s.register_data(Data(std::move(am), DataKind::XData));
+        }
+        const std::vector<Launch> plan = bake_fft_plan(nx, ny, C * F, true);
+        const uint32_t conj = 1;
+        std::vector<std::byte> cep_params(4);
+        std::memcpy(cep_params.data(), &conj, 4);
+        const uint64_t n = nx * ny * C * F;
+        double total = 0;
+        for (int r = 0; r < reps; ++r) {
+            const double a = now_s();
+            std::vector<NDArray> ak;
+            ak.push_back(c64({nx, ny, C, F}, Y));
+            DataHandle hk = s.register_data(Data(std::move(ak), DataKind::KData));
+            for (const Launch& l : plan)
+                s.launch_kernel("fft_radix2_pass", l.gather ? hk : hx, hx, l.params, l.gsize);
+            if (method == 0) {
+                s.launch_kernel("complex_element_prod", hx, hp, cep_params, n);
+                s.launch_kernel("ximage_sum", hp, hm, {}, nx * ny * F);
+            } else {
+                s.launch_kernel("rss_combine", hx, hm, {}, nx * ny * F);
+            }
+            Data res = s.fetch_data(hm);
+            std::memcpy(out, res.arrays[0].bytes().data(), res.arrays[0].byte_size());
+            s.release_data(hk);
+            total += now_s() - a;
+        }
+        *mean_s = reps > 0 ? total / reps : 0.0;
+    });
+}
+
 // Layout header bytes exactly as the reference serializes them
 // (src/layout.cpp:89-102) for a Data of `count` arrays.
 int refdrv_layout_header(int count, const int* types, const int* ranks, const uint64_t* dims8,

@@ -128,32 +128,55 @@ __device__ __forceinline__ void dft_regs(float2 (&v)[R]) {
     }
 }
 
+// Visits the line positions j + T*ms in increasing ms with the register
+// slot m that pairs with it: m = ms, or m = (ms + R/2) mod R when `rot` (a
+// cyclic shift by N/2 along the line, i.e. fftshift/ifftshift for even N;
+// the rotation is an involution so the pairing is symmetric).  Both branches
+// keep compile-time slot offsets, so addresses stay affine.
+template <int R, class F>
+__device__ __forceinline__ void slots(bool rot, F&& fn) {
+    if (rot)
+        sfor<R>([&](auto ms) { fn(std::integral_constant<int, (ms.value + R / 2) % R>{}, ms); });
+    else
+        sfor<R>([&](auto ms) { fn(ms, ms); });
+}
+
 // ---- per-size plan ------------------------------------------------------------------------
 
-// Radix lists: first radix == R (points per thread), product == N.
-template <int N> struct Plan;
-template <> struct Plan<1>    { static constexpr int R = 1;  static constexpr int P = 0; static constexpr int rad[1] = {1}; };
-template <> struct Plan<2>    { static constexpr int R = 2;  static constexpr int P = 1; static constexpr int rad[1] = {2}; };
-template <> struct Plan<4>    { static constexpr int R = 4;  static constexpr int P = 1; static constexpr int rad[1] = {4}; };
-template <> struct Plan<8>    { static constexpr int R = 8;  static constexpr int P = 1; static constexpr int rad[1] = {8}; };
-template <> struct Plan<16>   { static constexpr int R = 16; static constexpr int P = 1; static constexpr int rad[1] = {16}; };
-template <> struct Plan<32>   { static constexpr int R = 8;  static constexpr int P = 2; static constexpr int rad[2] = {8, 4}; };
-template <> struct Plan<64>   { static constexpr int R = 8;  static constexpr int P = 2; static constexpr int rad[2] = {8, 8}; };
-template <> struct Plan<128>  { static constexpr int R = 16; static constexpr int P = 2; static constexpr int rad[2] = {16, 8}; };
-template <> struct Plan<256>  { static constexpr int R = 16; static constexpr int P = 2; static constexpr int rad[2] = {16, 16}; };
-template <> struct Plan<512>  { static constexpr int R = 16; static constexpr int P = 3; static constexpr int rad[3] = {16, 16, 2}; };
-template <> struct Plan<1024> { static constexpr int R = 16; static constexpr int P = 3; static constexpr int rad[3] = {16, 16, 4}; };
-template <> struct Plan<2048> { static constexpr int R = 16; static constexpr int P = 3; static constexpr int rad[3] = {16, 16, 8}; };
-template <> struct Plan<4096> { static constexpr int R = 16; static constexpr int P = 3; static constexpr int rad[3] = {16, 16, 16}; };
+// Radix lists are derived from (N, R): R points per thread, passes of radix R
+// while they divide the remaining length, then one remainder pass.  The
+// default R is 16 for N >= 128 (two passes at 256, one shared-memory
+// exchange) and 8 below; kernels may ask for R = 8 at N >= 128 (more passes,
+// fewer registers per thread).
+constexpr int default_points(int N) { return N <= 16 ? N : (N <= 64 ? 8 : 16); }
 
-template <int N>
+template <int N, int RQ>
+struct Plan {
+    static constexpr int R = RQ < N ? RQ : N;
+    static constexpr int count_passes() {
+        int n = N, p = 0;
+        while (n > 1) {
+            n = n >= R ? n / R : 1;
+            ++p;
+        }
+        return p;
+    }
+    static constexpr int P = count_passes();
+    static constexpr int radix(int p) {
+        int n = N;
+        for (int i = 0; i < p; ++i) n = n >= R ? n / R : 1;
+        return n >= R ? R : n;
+    }
+};
+
+template <int N, int RQ = default_points(N)>
 struct LineFFT {
-    using PL = Plan<N>;
+    using PL = Plan<N, RQ>;
     static constexpr int R = PL::R;
     static constexpr int T = N / R;
     static constexpr int P = PL::P;
 
-    static constexpr int radix(int p) { return PL::rad[p]; }
+    static constexpr int radix(int p) { return PL::radix(p); }
     static constexpr int ns(int p) { return p == 0 ? 1 : ns(p - 1) * radix(p - 1); }
     // twiddle registers needed by pass p (p >= 1) and their offset
     static constexpr int tw_count(int p) { return p == 0 ? 0 : (R / radix(p)) * (radix(p) - 1); }
@@ -165,8 +188,10 @@ struct LineFFT {
     static constexpr int padded_len = N + (N >> 4);
 
     // Loads this thread's pass twiddles from the W_N^t table (DIR applied).
+    // The last pass' twiddles are pre-multiplied by `scale` so run() applies
+    // the normalisation for free (only the q = 0 slots need an explicit FMUL).
     __device__ __forceinline__ static void load_twiddles(float2 (&tw)[NTW], const float2* __restrict__ table,
-                                                         int j) {
+                                                         int j, float scale = 1.0f) {
         sfor<P>([&](auto pc) {
             constexpr int p = pc.value;
             if constexpr (p >= 1) {
@@ -177,7 +202,9 @@ struct LineFFT {
                     const int gm = g % Ns;
                     sfor<Rp - 1>([&](auto qc) {
                         constexpr int q = qc.value + 1;
-                        tw[tw_offset(p) + sc.value * (Rp - 1) + qc.value] = __ldg(&table[gm * q * stride]);
+                        float2 w = __ldg(&table[gm * q * stride]);
+                        if constexpr (p == P - 1) w = make_float2(w.x * scale, w.y * scale);
+                        tw[tw_offset(p) + sc.value * (Rp - 1) + qc.value] = w;
                     });
                 });
             }
@@ -186,9 +213,11 @@ struct LineFFT {
 
     // Runs all passes.  `line` is this line's shared buffer (padded_len
     // float2), `sync` a callable that synchronises the threads of the line.
+    // The output is multiplied by `scale`, which must be the value the
+    // twiddles were loaded with.
     template <int DIR, class Sync>
     __device__ __forceinline__ static void run(float2 (&v)[R], const float2 (&tw)[NTW], float2* line, int j,
-                                               Sync&& sync) {
+                                               Sync&& sync, float scale = 1.0f) {
         sfor<P>([&](auto pc) {
             constexpr int p = pc.value;
             constexpr int Rp = radix(p), Ns = ns(p), S = R / Rp;
@@ -211,9 +240,19 @@ struct LineFFT {
                     });
                 });
             }
+            if constexpr (p == P - 1) {
+                if (scale != 1.0f) {
+                    if constexpr (p == 0)
+                        sfor<R>([&](auto m) { v[m.value] = cscale(v[m.value], scale); });
+                    else  // q = 0 slots; the others went through scaled twiddles
+                        sfor<S>([&](auto sc) { v[sc.value] = cscale(v[sc.value], scale); });
+                }
+            }
             sfor<S>([&](auto sc) { dft_regs<Rp, DIR, S, sc.value>(v); });
             (void)Ns;
         });
+        if constexpr (P == 0)
+            if (scale != 1.0f) v[0] = cscale(v[0], scale);
     }
 };
 

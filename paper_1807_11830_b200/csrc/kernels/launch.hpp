@@ -80,13 +80,16 @@ struct LaunchShape {
     int block = 0;
     int grid = 0;
     int smem = 0;
-    int variant = 0;  // combine kernel variant (fp32 acc / register prefetch)
+    int variant = 0;  // combine kernel variant (bit0 fp32 acc, bit1 prefetch, bit2 8 pts/thread)
+    int rq = 0;       // points per thread of the chosen instantiation
 };
 
 // Pick block/grid/smem for a given problem (called once at init, baked into
 // the process' CUDA graph).
 LaunchShape plan_strided(std::uint64_t N, std::uint64_t nx, std::uint64_t planes, int device_sms);
-LaunchShape plan_contig(std::uint64_t N, Combine mode, std::uint64_t items, int device_sms);
+// variant (combine modes only): bit 0 fp32 accumulators, bit 1 register
+// prefetch, bit 2 eight points per thread; -1 = HETRECO_COMBINE_VARIANT or 3.
+LaunchShape plan_contig(std::uint64_t N, Combine mode, std::uint64_t items, int device_sms, int variant = -1);
 
 cudaError_t launch_strided(std::uint64_t N, int dir, const StridedArgs& a, const LaunchShape& s,
                            cudaStream_t stream);

@@ -635,8 +635,8 @@ class Process:
     def profile(self, reps: int = 5):
         """Mean device seconds of each kernel of this process (record order)."""
         n = C.c_int()
-        buf = (C.c_double * 16)()
-        _ck(lib().hetreco_process_profile(self._h, reps, buf, 16, C.byref(n)))
+        buf = (C.c_double * 4096)()
+        _ck(lib().hetreco_process_profile(self._h, reps, buf, 4096, C.byref(n)))
         return [buf[i] for i in range(n.value)]
 
     def stats(self) -> LaunchStats:

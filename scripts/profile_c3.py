@@ -1,7 +1,7 @@
 """Run the C3 SENSE (or RSS) recon a few times; print per-kernel device times.
 
 Used under ncu (kernel captures) and for variant sweeps:
-    HETRECO_COMBINE_VARIANT=1 python scripts/profile_c3.py --reps 20
+    HETRECO_COMBINE_VARIANT=1 HETRECO_CHUNK=2 python scripts/profile_c3.py --reps 20
 """
 import argparse
 import os
@@ -19,6 +19,7 @@ ap.add_argument("--coils", type=int, default=32)
 ap.add_argument("--frames", type=int, default=30)
 ap.add_argument("--launches", type=int, default=3)
 ap.add_argument("--reps", type=int, default=10)
+ap.add_argument("--timed", type=int, default=50, help="graph launches timed back to back")
 a = ap.parse_args()
 nx = ny = a.nx
 rng = np.random.default_rng(0)
@@ -38,9 +39,15 @@ for _ in range(a.launches):
 s.synchronize()
 if a.reps:
     t = p.profile(a.reps)
+    t1, t2 = sum(t[0::2]), sum(t[1::2])
     fy = nx * ny * a.coils * 8
     b1 = 2 * fy * a.frames
     b2 = fy * a.frames + (fy if a.method == "sens_recon" else 0) + nx * ny * a.frames * (8 if a.method == "sens_recon" else 4)
-    print(f"variant={os.environ.get('HETRECO_COMBINE_VARIANT', '0')} lpb={os.environ.get('HETRECO_LINES_PER_BLOCK', '128')} "
-          f"axis1 {t[0]*1e6:.1f} us {b1/t[0]/1e9:.0f} GB/s | axis0+combine {t[1]*1e6:.1f} us {b2/t[1]/1e9:.0f} GB/s "
-          f"| total {(t[0]+t[1])*1e6:.1f} us = {a.frames/(t[0]+t[1]):.0f} frames/s")
+    s.timer_start()
+    for _ in range(a.timed):
+        p.launch()
+    tg = s.timer_stop() / a.timed
+    print(f"{a.method} {nx}x{ny}x{a.coils}x{a.frames} variant={os.environ.get('HETRECO_COMBINE_VARIANT', '-')} "
+          f"chunk={os.environ.get('HETRECO_CHUNK', 'auto')} kernels={len(t)} | axis1 {t1*1e6:.1f} us {b1/t1/1e9:.0f} GB/s "
+          f"| axis0+combine {t2*1e6:.1f} us {b2/t2/1e9:.0f} GB/s | sum {(t1+t2)*1e6:.1f} us | graph {tg*1e6:.1f} us "
+          f"= {a.frames/tg:.0f} frames/s")

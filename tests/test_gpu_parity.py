@@ -298,6 +298,54 @@ def test_sens_recon_vs_oracle(s, dims):
     assert relmax(M, o.sens_recon(Y, S)) <= TOL
 
 
+@pytest.mark.parametrize("params", [{"accumulate": "fp64"}, {"accumulate": "fp64", "prefetch": False},
+                                    {"prefetch": False}, {"chunk_frames": 3}, {"chunk_frames": 1, "shift": False}],
+                         ids=lambda d: ",".join(f"{k}={v}" for k, v in d.items()))
+@pytest.mark.parametrize("method", ["sens_recon", "rss_recon"])
+def test_recon_variants_vs_oracle(s, params, method):
+    nx, ny, nc, nf = 256, 256, 6, 7
+    rng = np.random.default_rng(77)
+    Y = cplx(rng, nx, ny, nc, nf)
+    S = cplx(rng, nx, ny, nc)
+    if method == "sens_recon":
+        (M,), _ = run_process(s, method, [Y, S], [((nx, ny, nf), np.complex64)], params)
+        assert relmax(M, o.sens_recon(Y, S)) <= TOL
+    else:
+        (R,), _ = run_process(s, method, [Y], [((nx, ny, nf), np.float32)], params)
+        assert relmax(R, o.rss_recon(Y)) <= TOL
+
+
+def test_recon_fp64_accumulation_is_bitexact_combine(s):
+    """With fp64 accumulation the fused combine repeats ximage_sum's arithmetic
+    (fp32 products, fp64 coil-ordered sum): fed the same X it matches the
+    reference-ABI kernels bit for bit, so chain == fused up to the FFT only."""
+    rng = np.random.default_rng(78)
+    nx, ny, nc, nf = 64, 64, 5, 2
+    Y = cplx(rng, nx, ny, nc, nf)
+    S = cplx(rng, nx, ny, nc)
+    (M,), _ = run_process(s, "sens_recon", [Y, S], [((nx, ny, nf), np.complex64)], {"accumulate": "fp64"})
+    (X,), _ = run_process(s, "fft2d", [Y], [((nx, ny, nc, nf), np.complex64)], {"direction": "inverse"})
+    ref = o.ximage_sum(o.complex_element_prod(X, S, True))
+    assert relmax(M, ref) <= 1e-6
+
+
+def test_recon_rejects_bad_params(s):
+    Y = np.zeros((16, 16, 2, 1), np.complex64)
+    S = np.zeros((16, 16, 2), np.complex64)
+    hin = s.register_data(h.Data([Y, S], h.DataKind.KData))
+    hout = s.allocate_data([((16, 16, 1), np.complex64)])
+    with pytest.raises(h.InvalidParams):
+        h.Process(s, "sens_recon").set_input(hin).set_output(hout).init({"accumulate": "fp16"})
+    with pytest.raises(h.InvalidParams):
+        h.Process(s, "sens_recon").set_input(hin).set_output(hout).init({"chunk_frames": -1})
+    bad = s.allocate_data([((16, 8, 1), np.complex64)])
+    with pytest.raises(h.ShapeMismatch):
+        h.Process(s, "sens_recon").set_input(hin).set_output(bad).init()
+    smaps_wrong = s.register_data(h.Data([Y, np.zeros((16, 16, 3), np.complex64)], h.DataKind.KData))
+    with pytest.raises(h.ShapeMismatch):
+        h.Process(s, "sens_recon").set_input(smaps_wrong).set_output(hout).init()
+
+
 @pytest.mark.parametrize("dims", [(16, 8, 4, 3), (256, 256, 8, 1), (128, 32, 1, 4), (512, 512, 4, 1)],
                          ids=lambda t: "x".join(map(str, t)))
 def test_rss_recon_vs_oracle(s, dims):
