@@ -110,13 +110,8 @@ def dist_setup(n_gpus: int):
 
 
 def reduce_max(x: float, world: int) -> float:
-    if world == 1:
-        return x
-    import torch
-    import torch.distributed as dist
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    return float(t.item())
+    from paper_1807_11830_b200.sharding import max_over_ranks
+    return max_over_ranks(x) if world > 1 else x
 
 
 def barrier(world: int):

@@ -28,6 +28,13 @@
 extern "C" {
 #endif
 
+/* The library is built with -fvisibility=hidden: only this C-ABI is exported
+ * (its C++ internals share the hetreco:: namespace with the reference and
+ * must not interpose on a reference build loaded in the same process). */
+#if defined(__GNUC__)
+#pragma GCC visibility push(default)
+#endif
+
 /* ---- errors (include/hetreco/errors.hpp:12-219) ----------------------------- */
 #define HETRECO_OK 0
 const char* hetreco_last_error(void);
@@ -207,6 +214,10 @@ int hetreco_parse_layout_header(const void* bytes, uint64_t nbytes, hetreco_arra
                                 uint64_t* alignment, uint64_t* total_bytes);
 /* DeviceFilter::parse + describe (device.hpp:76-86) */
 int hetreco_filter_describe(const char* filter_text, char* buf, uint64_t cap);
+
+#if defined(__GNUC__)
+#pragma GCC visibility pop
+#endif
 
 #ifdef __cplusplus
 }

@@ -47,3 +47,20 @@ $CXX $FLAGS -c "$HERE/ref_driver.cpp" -o "$OUT/obj/ref_driver.o" & pids+=($!)
 for p in "${pids[@]}"; do wait "$p"; done
 $CXX -shared -o "$OUT/libhetreco_refdrv.so" "$OUT"/obj/*.o -ldl -lpthread
 echo "build_ref: wrote $OUT/libhetreco_refdrv.so"
+
+# Second flavour: the same reference library + driver, running on the B200
+# through the maintainer-side adapter integration/reference_cuda_backend.cpp
+# over libhetreco_b200.so's C-ABI (only when that library has been built).
+ROOT=$(cd "$HERE/.." && pwd)
+B200_LIB=$ROOT/paper_1807_11830_b200/libhetreco_b200.so
+if [ -f "$B200_LIB" ]; then
+  $CXX $FLAGS -DHETRECO_REF_ON_B200 -c "$HERE/ref_driver.cpp" -o "$OUT/ref_on_b200_driver.o" &
+  p1=$!
+  $CXX $FLAGS -I"$ROOT/include" -c "$ROOT/integration/reference_cuda_backend.cpp" -o "$OUT/reference_cuda_backend.o" &
+  p2=$!
+  wait $p1; wait $p2
+  REF_OBJS=$(ls "$OUT"/obj/*.o | grep -v ref_driver.o)
+  $CXX -shared -o "$OUT/libhetreco_ref_on_b200.so" $REF_OBJS "$OUT/ref_on_b200_driver.o" \
+    "$OUT/reference_cuda_backend.o" "$B200_LIB" -Wl,-rpath,'$ORIGIN/../../paper_1807_11830_b200' -ldl -lpthread
+  echo "build_ref: wrote $OUT/libhetreco_ref_on_b200.so"
+fi

@@ -27,6 +27,8 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 PORT_SO = os.path.join(HERE, "liboracle.so")
 REF_SO = os.path.join(HERE, "_ref", "libhetreco_refdrv.so")
+# the reference library on the B200 via integration/reference_cuda_backend.cpp
+REF_ON_B200_SO = os.path.join(HERE, "_ref", "libhetreco_ref_on_b200.so")
 
 # ElementType codes: include/hetreco/ndarray.hpp:17-24 (wire format)
 UINT8, INT32, FLOAT32, COMPLEX64, FLOAT64, COMPLEX128 = 1, 2, 3, 4, 5, 6
@@ -102,6 +104,50 @@ def reference():
             lib.refdrv_layout_header.argtypes = [_i32, _vp, _vp, _vp, _u64, _vp, C.POINTER(_u64)]
             _ref = lib
         return _ref
+
+
+class _RefOnB200:
+    """The unmodified reference session code on the CUDA adapter: the same
+    refdrv_* entry points, named refcuda_*."""
+
+    def __init__(self):
+        L = C.CDLL(REF_ON_B200_SO)
+        L.refcuda_last_error.restype = C.c_char_p
+        L.refcuda_run_kernel.argtypes = [C.c_char_p, _i32, _i32, _vp, _vp, _i32, _i32, _vp, _vp, _i32, _i32,
+                                         _vp, _vp, _i32, _vp, _u64, _u64]
+        L.refcuda_fft2d.argtypes = [_vp, _vp, _u64, _u64, _u64, _i32]
+        L.refcuda_recon.argtypes = [_i32, _vp, _vp, _vp, _u64, _u64, _u64, _u64, _i32, C.POINTER(_f64),
+                                    C.POINTER(_f64)]
+        self.L = L
+
+    def __getattr__(self, name):  # refdrv_x -> refcuda_x
+        return getattr(self.L, name.replace("refdrv_", "refcuda_"))
+
+
+_ref_b200 = None
+
+
+def ref_on_b200_available() -> bool:
+    return os.path.exists(REF_ON_B200_SO)
+
+
+def use_reference_on_b200():
+    """Context in which the ref_* helpers below run the reference's session
+    code on the B200 (integration adapter) instead of its CPU backend."""
+    import contextlib
+
+    @contextlib.contextmanager
+    def ctx():
+        global _ref, _ref_b200
+        saved = reference()
+        if _ref_b200 is None:
+            _ref_b200 = _RefOnB200()
+        _ref = _ref_b200
+        try:
+            yield
+        finally:
+            _ref = saved
+    return ctx()
 
 
 def _p(a: np.ndarray):

@@ -22,6 +22,19 @@
 #include "hetreco/backend.hpp"
 #include "hetreco/session.hpp"
 
+// Built twice by build_ref.sh: as libhetreco_refdrv.so on the reference CPU
+// backend (entry points refdrv_*), and with -DHETRECO_REF_ON_B200 as
+// libhetreco_ref_on_b200.so, where the SAME reference session code runs on the
+// B200 through integration/reference_cuda_backend.cpp (entry points refcuda_*).
+#ifdef HETRECO_REF_ON_B200
+#define REFDRV(name) refcuda_##name
+namespace hetreco_b200_integration {
+std::unique_ptr<hetreco::Backend> make_cuda_backend(int ordinal, std::uint64_t capacity);
+}
+#else
+#define REFDRV(name) refdrv_##name
+#endif
+
 using namespace hetreco;
 
 namespace {
@@ -31,7 +44,11 @@ using cf = std::complex<float>;
 thread_local std::string g_err;
 
 std::unique_ptr<Backend>& backend() {
+#ifdef HETRECO_REF_ON_B200
+    static std::unique_ptr<Backend> b = hetreco_b200_integration::make_cuda_backend(0, 0);
+#else
     static std::unique_ptr<Backend> b = make_reference_backend();
+#endif
     return b;
 }
 
@@ -121,10 +138,10 @@ int guarded(F&& f) {
 
 extern "C" {
 
-const char* refdrv_last_error() { return g_err.c_str(); }
+const char* REFDRV(last_error)() { return g_err.c_str(); }
 
 // WorkerPool size used by the reference backend (src/backend.cpp:73-79).
-int refdrv_pool_threads() {
+int REFDRV(pool_threads)() {
     unsigned hw = std::thread::hardware_concurrency();
     if (hw == 0) hw = 1;
     return int(hw > 16 ? 16 : hw);
@@ -133,7 +150,7 @@ int refdrv_pool_threads() {
 // Runs any builtin kernel once: in/out are single-array Data of the given
 // type/dims; `extra_in` (optional) is appended as array 1 of the input
 // (complex_element_prod's s).  Output array is overwritten with the result.
-int refdrv_run_kernel(const char* name, int in_type, int in_rank, const uint64_t* in_dims,
+int REFDRV(run_kernel)(const char* name, int in_type, int in_rank, const uint64_t* in_dims,
                       const void* in_data, int extra_type, int extra_rank,
                       const uint64_t* extra_dims, const void* extra_data, int out_type,
                       int out_rank, const uint64_t* out_dims, void* out_data, int in_place,
@@ -164,7 +181,7 @@ int refdrv_run_kernel(const char* name, int in_type, int in_rank, const uint64_t
 }
 
 // 2-D FFT of COMPLEX64 [nx, ny, batch] with the restated plan.
-int refdrv_fft2d(const float* in, float* out, uint64_t nx, uint64_t ny, uint64_t batch,
+int REFDRV(fft2d)(const float* in, float* out, uint64_t nx, uint64_t ny, uint64_t batch,
                  int inverse) {
     return guarded([&] {
         ComputeSession s(*backend());
@@ -187,7 +204,7 @@ int refdrv_fft2d(const float* in, float* out, uint64_t nx, uint64_t ny, uint64_t
 // Runs `reps` launches of the baked chain after one init; writes the last
 // result to `out` and the mean seconds per launch (each launch followed by
 // synchronize(), init excluded) to *mean_s, init seconds to *init_s.
-int refdrv_recon(int method, const float* Y, const float* S, void* out, uint64_t nx,
+int REFDRV(recon)(int method, const float* Y, const float* S, void* out, uint64_t nx,
                  uint64_t ny, uint64_t C, uint64_t F, int reps, double* mean_s,
                  double* init_s) {
     return guarded([&] {
@@ -248,7 +265,7 @@ int refdrv_recon(int method, const float* Y, const float* S, void* out, uint64_t
 // "send the data to the computing device", session.cpp:60-83), runs the
 // chain, fetches the images (session.cpp:85-98) and releases the k-space.
 // Writes the last result to `out`, mean seconds per step to *mean_s.
-int refdrv_recon_e2e(int method, const float* Y, const float* S, void* out, uint64_t nx, uint64_t ny,
+int REFDRV(recon_e2e)(int method, const float* Y, const float* S, void* out, uint64_t nx, uint64_t ny,
                      uint64_t C, uint64_t F, int reps, double* mean_s) {
     return guarded([&] {
         ComputeSession s(*backend());
@@ -300,7 +317,7 @@ int refdrv_recon_e2e(int method, const float* Y, const float* S, void* out, uint
 
 // Layout header bytes exactly as the reference serializes them
 // (src/layout.cpp:89-102) for a Data of `count` arrays.
-int refdrv_layout_header(int count, const int* types, const int* ranks, const uint64_t* dims8,
+int REFDRV(layout_header)(int count, const int* types, const int* ranks, const uint64_t* dims8,
                          uint64_t alignment, uint64_t* out_words, uint64_t* total_bytes) {
     return guarded([&] {
         std::vector<NDArray> arrs;

@@ -23,8 +23,9 @@ NVCC = os.path.join(CUDA, "bin", "nvcc")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-std=c++20", "--expt-relaxed-constexpr", "-O3", "-lineinfo", "-Xcompiler", "-fPIC",
+              "-Xcompiler", "-fvisibility=hidden",
               "-Xptxas", "-warn-spills", "-I", INCLUDE] + ARCH
-CXX_FLAGS = ["-std=c++20", "-O2", "-fPIC", "-Wall", "-Wno-unused-function", "-I", INCLUDE,
+CXX_FLAGS = ["-std=c++20", "-O2", "-fPIC", "-fvisibility=hidden", "-Wall", "-Wno-unused-function", "-I", INCLUDE,
              "-I", os.path.join(CUDA, "include")]
 
 
@@ -67,7 +68,8 @@ def build(force: bool = False, verbose: bool = True) -> str:
         objs = list(ex.map(lambda s: _compile(s, force, hm), cu + cpp))
     if force or not os.path.exists(LIB) or os.path.getmtime(LIB) < max(os.path.getmtime(o) for o in objs):
         tmp = LIB + f".{os.getpid()}.tmp"
-        cmd = [NVCC, "-shared", "-cudart", "static", "-o", tmp] + ARCH + objs + ["-lpthread", "-ldl", "-lrt"]
+        cmd = [NVCC, "-shared", "-cudart", "static", "-Xlinker", "-soname=libhetreco_b200.so", "-o", tmp] + ARCH + \
+            objs + ["-lpthread", "-ldl", "-lrt"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed: {' '.join(cmd)}\n{r.stdout}\n{r.stderr}")

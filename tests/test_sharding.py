@@ -1,0 +1,57 @@
+"""Multi-GPU host logic on CPU: frame slabs cover the frame axis exactly once
+with no overlap, and the only cross-rank exchange (max of the timing scalar)
+works over a world_size-2 gloo group (the same code path bench.py uses over
+NCCL)."""
+import os
+
+import pytest
+
+from paper_1807_11830_b200.sharding import frame_slab, imbalance, max_over_ranks, slab_bytes
+
+
+@pytest.mark.parametrize("world", [1, 2, 3, 4, 8])
+@pytest.mark.parametrize("frames", [1, 7, 30, 256])
+def test_slabs_partition_frames(world, frames):
+    covered = []
+    for r in range(world):
+        b, e = frame_slab(r, world, frames)
+        assert 0 <= b <= e <= frames
+        covered.extend(range(b, e))
+        assert abs((e - b) - frames / world) < 1
+    assert covered == list(range(frames))
+
+
+def test_c3_imbalance_and_bytes():
+    assert [frame_slab(r, 8, 30) for r in range(8)][0] == (0, 3)
+    assert abs(imbalance(8, 30) - (4 / 3.75 - 1)) < 1e-12
+    off, n = slab_bytes(4, 8, 256, 256, 32)
+    assert off == 4 * 256 * 256 * 32 * 8 and n == 4 * 256 * 256 * 32 * 8
+
+
+def _worker(rank, world, port, q):
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    b, e = frame_slab(rank, world, 30)
+    t = max_over_ranks(float(rank + 1) * 0.5)
+    q.put((rank, b, e, t))
+    dist.destroy_process_group()
+
+
+def test_gloo_world2_max_over_ranks():
+    import multiprocessing as mp
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    ps = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in ps)
+    for p in ps:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert [(b, e) for _, b, e, _ in res] == [(0, 15), (15, 30)]
+    assert all(t == 1.0 for *_, t in res)
