@@ -43,13 +43,15 @@ using cf = std::complex<float>;
 
 thread_local std::string g_err;
 
+// Process-lifetime backend, deliberately leaked (no static destructor runs
+// after the CUDA runtime has torn itself down at exit).
 std::unique_ptr<Backend>& backend() {
 #ifdef HETRECO_REF_ON_B200
-    static std::unique_ptr<Backend> b = hetreco_b200_integration::make_cuda_backend(0, 0);
+    static auto* b = new std::unique_ptr<Backend>(hetreco_b200_integration::make_cuda_backend(0, 0));
 #else
-    static std::unique_ptr<Backend> b = make_reference_backend();
+    static auto* b = new std::unique_ptr<Backend>(make_reference_backend());
 #endif
-    return b;
+    return *b;
 }
 
 std::vector<std::byte> fft_params(uint32_t mode, uint64_t L, uint64_t S, uint64_t m, float scale,

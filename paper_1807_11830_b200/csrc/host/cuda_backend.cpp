@@ -253,14 +253,17 @@ std::uint64_t CudaBackend::live_bytes() const {
 
 namespace {
 
-std::vector<std::unique_ptr<CudaBackend>>& owned() {
-    static std::vector<std::unique_ptr<CudaBackend>> list = [] {
-        std::vector<std::unique_ptr<CudaBackend>> v;
+// Backends live for the process lifetime (backend.hpp:81-85).  They are
+// intentionally never destroyed: at exit the CUDA runtime tears itself down
+// and stream/memory releases from static destructors would race with it.
+std::vector<CudaBackend*>& owned() {
+    static std::vector<CudaBackend*>* list = [] {
+        auto* v = new std::vector<CudaBackend*>;
         const int n = cuda_device_count();
-        for (int i = 0; i < n; ++i) v.push_back(std::make_unique<CudaBackend>(i));
+        for (int i = 0; i < n; ++i) v->push_back(new CudaBackend(i));
         return v;
     }();
-    return list;
+    return *list;
 }
 
 }  // namespace
@@ -268,7 +271,7 @@ std::vector<std::unique_ptr<CudaBackend>>& owned() {
 std::span<Backend* const> backend_snapshot() {
     static const std::vector<Backend*> ptrs = [] {
         std::vector<Backend*> v;
-        for (auto& b : owned()) v.push_back(b.get());
+        for (CudaBackend* b : owned()) v.push_back(b);
         return v;
     }();
     return ptrs;
