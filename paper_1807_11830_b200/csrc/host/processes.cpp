@@ -737,6 +737,9 @@ public:
         if (scratch_.size() != scratch_bytes) scratch_ = DevMem(scratch_bytes);
         const int ord = session().cuda().ordinal();
         plan_.make(nx_, ny_, +1, nc_ * chunk_, mode_, ny_ * chunk_, ord);
+        // prefetch form measured per size on B200: register copy at 256,
+        // ping-pong (two-way unrolled) at 512 (profiles/round1_summary.md)
+        if ((variant_ & 2) && !std::getenv("HETRECO_COMBINE_VARIANT") && nx_ != 512) variant_ |= 8;
         plan_.s2 = dev::plan_contig(nx_, mode_, ny_ * chunk_, sm_count(ord), variant_);
         const std::uint64_t tail = nf_ % chunk_;
         if (tail) {

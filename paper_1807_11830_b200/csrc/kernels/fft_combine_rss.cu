@@ -12,23 +12,20 @@ constexpr int M = 2;
 template <int N, int V>
 struct CombineK {
     static constexpr bool R8 = has_variants<N>() && (V & 4) && LineFFT<N>::R != 8;
-    static constexpr bool PF = has_variants<N>() && (V & 2);
+    // bit 1: prefetch; bit 3 selects the copy form over the ping-pong form
+    static constexpr int PF = (has_variants<N>() && (V & 2)) ? ((V & 8) ? 1 : 2) : 0;
     static constexpr auto kernel() {
         return &k_fft_combine<N, M, (V & 1) != 0, PF, R8 ? 8 : default_points(N)>;
     }
 };
 
-template <int N>
+template <int N, int V = 0>
 auto pick(int v) {
-    switch (v & 7) {
-        case 1: return CombineK<N, 1>::kernel();
-        case 2: return CombineK<N, 2>::kernel();
-        case 3: return CombineK<N, 3>::kernel();
-        case 4: return CombineK<N, 4>::kernel();
-        case 5: return CombineK<N, 5>::kernel();
-        case 6: return CombineK<N, 6>::kernel();
-        case 7: return CombineK<N, 7>::kernel();
-        default: return CombineK<N, 0>::kernel();
+    if constexpr (V == 15) {
+        return CombineK<N, 15>::kernel();
+    } else {
+        if ((v & 15) == V) return CombineK<N, V>::kernel();
+        return pick<N, V + 1>(v);
     }
 }
 

@@ -35,7 +35,7 @@ int contig_occ(int block, int smem) {
 LaunchShape plan_contig(std::uint64_t N, Combine mode, std::uint64_t items, int sms, int variant) {
     LaunchShape s;
     if (points_for(N, 0) == 0) return s;
-    s.variant = mode == Combine::None ? 0 : (variant >= 0 ? variant : env_int("HETRECO_COMBINE_VARIANT", 3));
+    s.variant = mode == Combine::None ? 0 : (variant >= 0 ? variant : env_int("HETRECO_COMBINE_VARIANT", N == 512 ? 3 : 11));
     const int R = points_for(N, (s.variant & 4) ? 8 : 0);
     s.rq = R;
     const int T = int(N) / R;

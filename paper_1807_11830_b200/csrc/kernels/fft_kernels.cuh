@@ -37,7 +37,7 @@ constexpr int line_stride() {
 // variant.  Indices are 32-bit and power-of-two divisions are shifts (a
 // 64-bit division is an emulated call on the GPU).
 
-template <int N, int DIR, int NXC, int RQ = default_points(N)>
+template <int N, int DIR, int NXC, int RQ = default_points(N), bool PFS = false>
 __global__ void __launch_bounds__(512) k_fft_strided(StridedArgs a, int tx, std::uint32_t ntiles) {
     using L = LineFFT<N, RQ>;
     constexpr int R = L::R, T = L::T;
@@ -53,23 +53,48 @@ __global__ void __launch_bounds__(512) k_fft_strided(StridedArgs a, int tx, std:
     const std::uint64_t plane_elems = std::uint64_t(nx) * N;
     const std::uint32_t step = std::uint32_t(T) * nx;  // slot-to-slot distance (runtime variant)
     const bool sh_in = a.shift_in, sh_out = a.shift_out;
-    for (std::uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    auto tile_off = [&](std::uint32_t tile) {
         const std::uint32_t plane = tile >> lx;
         const std::uint32_t col = (tile & (xtiles - 1)) * std::uint32_t(tx) + std::uint32_t(l);
-        const std::uint64_t off = std::uint64_t(plane) * plane_elems + col + std::uint32_t(j) * nx;
+        return std::uint64_t(plane) * plane_elems + col + std::uint32_t(j) * nx;
+    };
+    auto load = [&](std::uint64_t off, float2(&v)[R]) {
         const float2* src = a.in + off;
-        float2 v[R];
         if constexpr (NXC > 0) {
             slots<R>(sh_in, [&](auto m, auto ms) { v[m.value] = __ldcs(src + ms.value * T * NXC); });
         } else {
             slots<R>(sh_in, [&](auto m, auto ms) { v[m.value] = __ldcs(src + ms.value * step); });
         }
-        L::template run<DIR>(v, tw, line, j, [] { __syncthreads(); }, a.scale);
+    };
+    auto store = [&](std::uint64_t off, float2(&v)[R]) {
         float2* dst = a.out + off;
         if constexpr (NXC > 0) {
             slots<R>(sh_out, [&](auto m, auto ms) { dst[ms.value * T * NXC] = v[m.value]; });
         } else {
             slots<R>(sh_out, [&](auto m, auto ms) { dst[ms.value * step] = v[m.value]; });
+        }
+    };
+    if constexpr (PFS) {
+        // the next tile's column samples are in flight while this tile is
+        // transformed (tiles are disjoint, so in-place use stays safe)
+        float2 nxt[R];
+        std::uint32_t tile = blockIdx.x;
+        if (tile < ntiles) load(tile_off(tile), nxt);
+        for (; tile < ntiles; tile += gridDim.x) {
+            float2 v[R];
+            sfor<R>([&](auto m) { v[m.value] = nxt[m.value]; });
+            const std::uint64_t off = tile_off(tile);
+            if (tile + gridDim.x < ntiles) load(tile_off(tile + gridDim.x), nxt);
+            L::template run<DIR>(v, tw, line, j, [] { __syncthreads(); }, a.scale);
+            store(off, v);
+        }
+    } else {
+        for (std::uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+            float2 v[R];
+            const std::uint64_t off = tile_off(tile);
+            load(off, v);
+            L::template run<DIR>(v, tw, line, j, [] { __syncthreads(); }, a.scale);
+            store(off, v);
         }
     }
 }
@@ -116,7 +141,9 @@ __global__ void __launch_bounds__(256) k_fft_contig(ContigArgs a, int lpb, std::
 // fp32 instead of fp64 accumulators; PF double-buffers the next coil's X and
 // S in registers so their HBM/L2 latency overlaps the current coil's FFT.
 
-template <int N, int MODE, bool ACCF, bool PF, int RQ = default_points(N)>
+// PF: 0 = no prefetch, 1 = next coil copied into registers at the top of each
+// iteration, 2 = ping-pong register buffers (loop unrolled by two).
+template <int N, int MODE, bool ACCF, int PF, int RQ = default_points(N)>
 __global__ void __launch_bounds__(256) k_fft_combine(ContigArgs a, int lpb, std::uint32_t items) {
     using L = LineFFT<N, RQ>;
     constexpr int R = L::R, T = L::T;
@@ -192,7 +219,23 @@ __global__ void __launch_bounds__(256) k_fft_combine(ContigArgs a, int lpb, std:
                 });
             }
         };
-        if constexpr (PF) {
+        if constexpr (PF == 1) {
+            float2 xn[R];
+            SBuf sn;
+            load_x(0, xn);
+            if constexpr (SENSE) load_s(0, sn);
+            for (std::uint32_t c = 0; c < C; ++c) {
+                float2 v[R];
+                SBuf sv;
+                sfor<R>([&](auto m) { v[m.value] = xn[m.value]; });
+                if constexpr (SENSE) sfor<R>([&](auto m) { sv[m.value] = sn[m.value]; });
+                if (c + 1 < C) {
+                    load_x(c + 1, xn);
+                    if constexpr (SENSE) load_s(c + 1, sn);
+                }
+                process(v, sv, c);
+            }
+        } else if constexpr (PF == 2) {
             // ping-pong register buffers: coil c+1 is in flight while c is transformed
             float2 xa[R], xb[R];
             SBuf sa, sb;

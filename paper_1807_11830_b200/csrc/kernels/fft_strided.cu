@@ -8,7 +8,13 @@ bool fft_size_supported(std::uint64_t n) { return points_for(n, 0) != 0; }
 namespace {
 
 template <int N, int RQ>
-int strided_occ(int block, int smem) {
+int strided_occ(int block, int smem, int variant) {
+    if constexpr (has_variants<N>()) {
+        if (variant & 1) {
+            blocks_per_sm(k_fft_strided<N, -1, N, RQ, true>, block, smem);
+            return blocks_per_sm(k_fft_strided<N, 1, N, RQ, true>, block, smem);
+        }
+    }
     blocks_per_sm(k_fft_strided<N, -1, N, RQ>, block, smem);
     blocks_per_sm(k_fft_strided<N, -1, 0, RQ>, block, smem);
     blocks_per_sm(k_fft_strided<N, 1, N, RQ>, block, smem);
@@ -18,6 +24,15 @@ int strided_occ(int block, int smem) {
 template <int N, int RQ>
 void strided_go(int dir, bool sq, const StridedArgs& a, const LaunchShape& s, int tx, std::uint32_t tiles,
                 cudaStream_t st) {
+    if constexpr (has_variants<N>()) {
+        if (sq && (s.variant & 1)) {  // register prefetch of the next tile (square fast path)
+            if (dir > 0)
+                k_fft_strided<N, 1, N, RQ, true><<<s.grid, s.block, s.smem, st>>>(a, tx, tiles);
+            else
+                k_fft_strided<N, -1, N, RQ, true><<<s.grid, s.block, s.smem, st>>>(a, tx, tiles);
+            return;
+        }
+    }
     if (dir > 0) {
         if (sq)
             k_fft_strided<N, 1, N, RQ><<<s.grid, s.block, s.smem, st>>>(a, tx, tiles);
@@ -35,10 +50,13 @@ void strided_go(int dir, bool sq, const StridedArgs& a, const LaunchShape& s, in
 
 LaunchShape plan_strided(std::uint64_t N, std::uint64_t nx, std::uint64_t planes, int sms) {
     LaunchShape s;
-    const int rq = env_int("HETRECO_STRIDED_POINTS", 0);
+    // measured defaults (profiles/round1_summary.md): 512-point columns run
+    // best with 8 points/thread, 8-column tiles and next-tile prefetch.
+    const int rq = env_int("HETRECO_STRIDED_POINTS", N == 512 ? 8 : 0);
     const int R = points_for(N, rq);
     if (R == 0) return s;
     s.rq = R;
+    s.variant = env_int("HETRECO_STRIDED_PF", N == 512 ? 1 : 0);
     const int T = int(N) / R;
     const int ls_bytes = stride_of(N) * 8;
     // columns per tile: >= 16 (128-B rows) when possible, bounded by 512
@@ -46,7 +64,7 @@ LaunchShape plan_strided(std::uint64_t N, std::uint64_t nx, std::uint64_t planes
     std::uint64_t tx = std::max(16, 256 / T);
     tx = std::min<std::uint64_t>(tx, std::uint64_t(std::max(1, 512 / T)));
     tx = std::min<std::uint64_t>(tx, std::uint64_t(std::max(1, (100 * 1024) / ls_bytes)));
-    if (const int e = env_int("HETRECO_STRIDED_TX", 0)) tx = std::uint64_t(e);
+    if (const int e = env_int("HETRECO_STRIDED_TX", N == 512 ? 8 : 0)) tx = std::uint64_t(e);
     tx = std::min<std::uint64_t>(tx, nx);
     while (tx > 1 && nx % tx) tx >>= 1;  // both powers of two in practice
     s.block = int(tx) * T;
@@ -58,10 +76,10 @@ LaunchShape plan_strided(std::uint64_t N, std::uint64_t nx, std::uint64_t planes
     case n:                                                               \
         if constexpr (has_variants<n>())                                  \
             if (R == 8 && LineFFT<n>::R != 8) {                           \
-                occ = strided_occ<n, 8>(s.block, s.smem);                 \
+                occ = strided_occ<n, 8>(s.block, s.smem, s.variant);                 \
                 break;                                                    \
             }                                                             \
-        occ = strided_occ<n, default_points(n)>(s.block, s.smem);         \
+        occ = strided_occ<n, default_points(n)>(s.block, s.smem, s.variant);         \
         break;
         HETRECO_FFT_SIZES(X)
 #undef X
