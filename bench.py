@@ -280,6 +280,19 @@ def run_ours(args):
         # streamed result equals the resident process output
         M_dev = s.fetch_data(hout).arrays[0]
         e2e["matches_resident"] = bool(np.abs(M_dev - Mp).max() <= 1e-5 * np.abs(M_dev).max())
+        # host-link roofline: plain pinned H2D copy of the same bytes on this box
+        link = h.CudaBackend(local)
+        buf = link.allocate(Yp.nbytes)
+        link.upload(buf, 0, Yp.reshape(-1, order="F").view(np.uint8))
+        t0 = time.perf_counter()
+        for _ in range(3):
+            link.upload(buf, 0, Yp.reshape(-1, order="F").view(np.uint8))
+        link_gbs = 3 * Yp.nbytes / (time.perf_counter() - t0) / 1e9
+        link.release(buf)
+        link.close()
+        e2e["host_link_peak_gbs"] = link_gbs
+        e2e["host_link_frac"] = e2e["host_link_gbs"] / link_gbs
+        e2e["host_link_roofline_frames_per_s"] = NF * world * link_gbs * 1e9 / (FRAME_Y * NF)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -15,12 +15,14 @@ struct CombineK {
     // bit 1: prefetch; bit 3 selects the copy form over the ping-pong form
     static constexpr int PF = (has_variants<N>() && (V & 2)) ? ((V & 8) ? 1 : 2) : 0;
     static constexpr auto kernel() {
-        return &k_fft_combine<N, M, (V & 1) != 0, PF, R8 ? 8 : default_points(N)>;
+        return &k_fft_combine<N, M, (V & 1) != 0, PF, R8 ? 8 : default_points(N), (V & 16) ? 3 : 1>;
     }
 };
 
 template <int N, int V = 0>
 auto pick(int v) {
+    if constexpr (V == 0)
+        if (has_variants<N>() && (v & 31) == 27) return CombineK<N, 27>::kernel();  // copy-PF fp32, 3 CTAs/SM
     if constexpr (V == 15) {
         return CombineK<N, 15>::kernel();
     } else {

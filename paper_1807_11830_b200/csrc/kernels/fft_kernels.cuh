@@ -37,8 +37,9 @@ constexpr int line_stride() {
 // variant.  Indices are 32-bit and power-of-two divisions are shifts (a
 // 64-bit division is an emulated call on the GPU).
 
-template <int N, int DIR, int NXC, int RQ = default_points(N), bool PFS = false>
-__global__ void __launch_bounds__(512) k_fft_strided(StridedArgs a, int tx, std::uint32_t ntiles) {
+// MINB > 1 asks ptxas for MINB resident 256-thread CTAs per SM (register cap).
+template <int N, int DIR, int NXC, int RQ = default_points(N), bool PFS = false, int MINB = 1>
+__global__ void __launch_bounds__(MINB > 1 ? 256 : 512, MINB > 1 ? MINB : 0) k_fft_strided(StridedArgs a, int tx, std::uint32_t ntiles) {
     using L = LineFFT<N, RQ>;
     constexpr int R = L::R, T = L::T;
     extern __shared__ float2 smem[];
@@ -143,8 +144,8 @@ __global__ void __launch_bounds__(256) k_fft_contig(ContigArgs a, int lpb, std::
 
 // PF: 0 = no prefetch, 1 = next coil copied into registers at the top of each
 // iteration, 2 = ping-pong register buffers (loop unrolled by two).
-template <int N, int MODE, bool ACCF, int PF, int RQ = default_points(N)>
-__global__ void __launch_bounds__(256) k_fft_combine(ContigArgs a, int lpb, std::uint32_t items) {
+template <int N, int MODE, bool ACCF, int PF, int RQ = default_points(N), int MINB = 1>
+__global__ void __launch_bounds__(MINB > 1 ? 128 : 256, MINB > 1 ? MINB : 0) k_fft_combine(ContigArgs a, int lpb, std::uint32_t items) {
     using L = LineFFT<N, RQ>;
     constexpr int R = L::R, T = L::T;
     constexpr bool SENSE = MODE == int(Combine::Sense);

@@ -10,6 +10,10 @@ namespace {
 template <int N, int RQ>
 int strided_occ(int block, int smem, int variant) {
     if constexpr (has_variants<N>()) {
+        if ((variant & 2) && !(variant & 1)) {
+            blocks_per_sm(k_fft_strided<N, -1, N, RQ, false, 3>, block, smem);
+            return blocks_per_sm(k_fft_strided<N, 1, N, RQ, false, 3>, block, smem);
+        }
         if (variant & 1) {
             blocks_per_sm(k_fft_strided<N, -1, N, RQ, true>, block, smem);
             return blocks_per_sm(k_fft_strided<N, 1, N, RQ, true>, block, smem);
@@ -25,6 +29,13 @@ template <int N, int RQ>
 void strided_go(int dir, bool sq, const StridedArgs& a, const LaunchShape& s, int tx, std::uint32_t tiles,
                 cudaStream_t st) {
     if constexpr (has_variants<N>()) {
+        if (sq && (s.variant & 2) && !(s.variant & 1)) {  // 3 CTAs/SM register cap
+            if (dir > 0)
+                k_fft_strided<N, 1, N, RQ, false, 3><<<s.grid, s.block, s.smem, st>>>(a, tx, tiles);
+            else
+                k_fft_strided<N, -1, N, RQ, false, 3><<<s.grid, s.block, s.smem, st>>>(a, tx, tiles);
+            return;
+        }
         if (sq && (s.variant & 1)) {  // register prefetch of the next tile (square fast path)
             if (dir > 0)
                 k_fft_strided<N, 1, N, RQ, true><<<s.grid, s.block, s.smem, st>>>(a, tx, tiles);
@@ -56,7 +67,8 @@ LaunchShape plan_strided(std::uint64_t N, std::uint64_t nx, std::uint64_t planes
     const int R = points_for(N, rq);
     if (R == 0) return s;
     s.rq = R;
-    s.variant = env_int("HETRECO_STRIDED_PF", N == 512 ? 1 : 0);
+    // bit 0 next-tile prefetch (512), bit 1 three CTAs per SM register cap (256)
+    s.variant = env_int("HETRECO_STRIDED_PF", N == 512 ? 1 : (N == 256 ? 2 : 0));
     const int T = int(N) / R;
     const int ls_bytes = stride_of(N) * 8;
     // columns per tile: >= 16 (128-B rows) when possible, bounded by 512
