@@ -201,7 +201,9 @@ std::unique_ptr<GraphProcess> make_sens_recon(ComputeSession& s, std::string nam
 std::unique_ptr<GraphProcess> make_rss_recon(ComputeSession& s, std::string name = "rss_recon");
 
 // Factory by kind name ("negate", "fft2d", "complex_element_prod",
-// "ximage_sum", "rss_combine", "sens_recon", "rss_recon").
+// "ximage_sum", "rss_combine", "sens_recon", "rss_recon", and the SENSE model
+// "sense_forward" (E m = P F (S m), input [M, S(, mask)] -> k-space
+// [nx,ny,C,F]) / "sense_normal" (E^H E m -> [nx,ny,F]); square images).
 std::unique_ptr<GraphProcess> make_process(ComputeSession& s, std::string_view kind, std::string name = {});
 
 // ---- host-streamed reconstruction (paper's pinned/mapped streaming) ------------------------

@@ -219,6 +219,25 @@ int oracle_sens_recon(const float* Y, const float* S, float* M, uint64_t nx, uin
     return 0;
 }
 
+int oracle_sense_forward(const float* M, const float* S, const float* mask, float* Y, uint64_t nx,
+                         uint64_t ny, uint64_t C, uint64_t F, float* scratch) {
+    const uint64_t plane = nx * ny;
+    for (uint64_t f = 0; f < F; ++f) {
+        for (uint64_t c = 0; c < C; ++c) {
+            /* S_c . M_f (complex_element_prod, conjugate = 0) */
+            oracle_complex_element_prod(M + 2 * plane * f, plane, S + 2 * plane * c, plane, scratch, 0);
+            float* y = Y + 2 * plane * (c + C * f);
+            if (oracle_fft2d(scratch, y, nx, ny, 1, 0) != 0) return -1;
+            if (mask)
+                for (uint64_t p = 0; p < plane; ++p) {
+                    y[2 * p] *= mask[p];
+                    y[2 * p + 1] *= mask[p];
+                }
+        }
+    }
+    return 0;
+}
+
 int oracle_rss_recon(const float* Y, float* R, uint64_t nx, uint64_t ny, uint64_t C,
                      uint64_t F, float* scratch) {
     if (oracle_fft2d(Y, scratch, nx, ny, C * F, 1) != 0) return -1;

@@ -72,6 +72,14 @@ int oracle_sens_recon(const float* Y, const float* S, float* M, uint64_t nx, uin
 int oracle_rss_recon(const float* Y, float* R, uint64_t nx, uint64_t ny, uint64_t C,
                      uint64_t F, float* scratch);
 
+/* SENSE forward model (no reference kernel exists; composed from the
+ * reference's own operations): Y[:,:,c,f] = mask . fft2d_FORWARD(S_c . M_f),
+ * S_c . M_f as complex_element_prod (conj = 0, complex_element_prod.cl.src:9-19),
+ * mask FLOAT32 [nx,ny] or NULL.  M [nx,ny,F], S [nx,ny,C], Y [nx,ny,C,F].
+ * `scratch` holds nx*ny complex values. */
+int oracle_sense_forward(const float* M, const float* S, const float* mask, float* Y, uint64_t nx,
+                         uint64_t ny, uint64_t C, uint64_t F, float* scratch);
+
 #ifdef __cplusplus
 }
 #endif

@@ -78,6 +78,7 @@ def port():
             lib.oracle_matrix_add_f32.argtypes = [_vp, _vp, _vp, _u64]
             lib.oracle_sens_recon.argtypes = [_vp, _vp, _vp, _u64, _u64, _u64, _u64, _vp]
             lib.oracle_rss_recon.argtypes = [_vp, _vp, _u64, _u64, _u64, _u64, _vp]
+            lib.oracle_sense_forward.argtypes = [_vp, _vp, _vp, _vp, _u64, _u64, _u64, _u64, _vp]
             _port = lib
         return _port
 
@@ -251,6 +252,28 @@ def rss_recon(Y) -> np.ndarray:
     if port().oracle_rss_recon(_p(Y), _p(R), nx, ny, nc, nf, _p(scratch)) != 0:
         raise ValueError("rss_recon: dims must be powers of two")
     return R
+
+
+def sense_forward(M, S, mask=None) -> np.ndarray:
+    """Y[:,:,c,f] = mask . FFT2_forward(S_c . M_f) (no reference kernel; composed
+    from complex_element_prod + the restated FFT plan)."""
+    M = _f(M, np.complex64)
+    S = _f(S, np.complex64)
+    nx, ny = M.shape[:2]
+    nf = M.size // (nx * ny)
+    nc = S.size // (nx * ny)
+    Y = np.empty((nx, ny, nc, nf), np.complex64, order="F")
+    mk = _f(mask, np.float32) if mask is not None else None
+    scratch = np.empty(nx * ny, np.complex64)
+    if port().oracle_sense_forward(_p(M), _p(S), _p(mk) if mk is not None else None, _p(Y), nx, ny, nc, nf,
+                                   _p(scratch)) != 0:
+        raise ValueError("sense_forward: dims must be powers of two")
+    return Y
+
+
+def sense_normal(M, S, mask=None) -> np.ndarray:
+    """E^H E M = sens_recon(sense_forward(M, S, mask), S)."""
+    return sens_recon(sense_forward(M, S, mask), S)
 
 
 # ---------------------------------------------------------------------------

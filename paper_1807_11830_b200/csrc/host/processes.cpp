@@ -778,6 +778,87 @@ private:
     dev::LaunchShape tail_s1_, tail_s2_;
 };
 
+// SENSE forward model E m = P F (S m) ("sense_forward") and the normal
+// operator E^H E m ("sense_normal", the iterative-reconstruction kernel of
+// expand + forward x-FFT, y-FFT / mask / inverse y-FFT in
+// registers, inverse x-FFT + conj(S) coil combine).  Input Data:
+// [M [nx,ny,F], S [nx,ny,C] (, mask FLOAT32 [nx,ny])].
+class SenseModelProcess final : public GraphProcess {
+public:
+    SenseModelProcess(ComputeSession& s, std::string name, bool normal)
+        : GraphProcess(s, std::move(name)), normal_(normal) {}
+    void bake(const ProcessParams& p) override {
+        p.require_known({"shift"});
+        shift_ = p.get_bool("shift", false);
+        const LayoutDescriptor& li = input_layout();
+        const LayoutRecord& m = array_of(li, 0, name());
+        const LayoutRecord& sm = array_of(li, 1, name());
+        require_type(m, ElementType::Complex64, name());
+        require_type(sm, ElementType::Complex64, name());
+        nx_ = m.dims[0];
+        ny_ = m.rank > 1 ? m.dims[1] : 1;
+        nf_ = prod(m, 2, m.rank);
+        if (nx_ != ny_ || !is_pow2(nx_) || !dev::fft_size_supported(nx_))
+            throw ShapeMismatch(name() + ": images must be square with a power-of-two side <= 4096, got " +
+                                dims_str(m));
+        if (sm.dims[0] != nx_ || sm.dims[1] != ny_)
+            throw ShapeMismatch(name() + ": sensitivity maps " + dims_str(sm) + " do not match image " + dims_str(m));
+        nc_ = prod(sm, 2, sm.rank);
+        mask_ = nullptr;
+        if (li.records.size() > 2) {
+            const LayoutRecord& mk = li.records[2];
+            require_type(mk, ElementType::Float32, name());
+            if (mk.element_count() != nx_ * ny_)
+                throw ShapeMismatch(name() + ": mask " + dims_str(mk) + " must be [nx, ny]");
+            mask_ = static_cast<const float*>(session().device_array(require_input(), 2));
+        }
+        const LayoutRecord& o = array_of(output_layout(), 0, name());
+        require_type(o, ElementType::Complex64, name());
+        const std::uint64_t want = normal_ ? nx_ * ny_ * nf_ : nx_ * ny_ * nc_ * nf_;
+        if (o.dims[0] != nx_ || o.element_count() != want)
+            throw ShapeMismatch(name() + ": output " + dims_str(o) + (normal_ ? " must be [nx, ny, frames]"
+                                                                             : " must be [nx, ny, coils, frames]"));
+        m_ = static_cast<const float2*>(session().device_array(require_input(), 0));
+        s_ = static_cast<const float2*>(session().device_array(require_input(), 1));
+        out_ = static_cast<float2*>(session().device_array(require_output(), 0));
+        const int ord = session().cuda().ordinal(), sms = sm_count(ord);
+        tw_fwd_ = twiddle_table(nx_, -1);
+        s_exp_ = dev::plan_expand(nx_, ny_ * nc_ * nf_, sms);
+        s_col_ = dev::plan_strided_masked(ny_, normal_, nc_ * nf_, sms);
+        if (normal_) {
+            tw_inv_ = twiddle_table(nx_, +1);
+            if (scratch_.size() != nx_ * ny_ * nc_ * nf_ * 8) scratch_ = DevMem(nx_ * ny_ * nc_ * nf_ * 8);
+            s_comb_ = dev::plan_contig(nx_, dev::Combine::Sense, ny_ * nf_, sms);
+        }
+    }
+    void record(cudaStream_t s) override {
+        float2* z = normal_ ? scratch_.as<float2>() : out_;
+        dev::ContigArgs ae{m_, z, s_, ny_, nc_, nf_, shift_, shift_, 1.0f, tw_fwd_.as<float2>()};
+        ck(dev::launch_expand(nx_, ae, s_exp_, s), name() + "/expand+x-fft");
+        mark(s);
+        dev::StridedArgs ac{z, z, nx_, nc_ * nf_, shift_, shift_, 1.0f, tw_fwd_.as<float2>(), mask_};
+        ck(dev::launch_strided_masked(ny_, normal_, ac, s_col_, s), name() + (normal_ ? "/y-fft.mask.y-ifft" : "/y-fft.mask"));
+        mark(s);
+        if (normal_) {
+            dev::ContigArgs ar{z, out_, s_, ny_, nc_, nf_, shift_, shift_, float(1.0 / (double(nx_) * double(ny_))),
+                               tw_inv_.as<float2>()};
+            ck(dev::launch_contig(nx_, +1, dev::Combine::Sense, ar, s_comb_, s), name() + "/x-ifft+combine");
+            mark(s);
+        }
+    }
+
+private:
+    bool normal_;
+    bool shift_ = false;
+    std::uint64_t nx_ = 0, ny_ = 0, nc_ = 0, nf_ = 0;
+    const float2* m_ = nullptr;
+    const float2* s_ = nullptr;
+    const float* mask_ = nullptr;
+    float2* out_ = nullptr;
+    DevMem tw_fwd_, tw_inv_, scratch_;
+    dev::LaunchShape s_exp_, s_col_, s_comb_;
+};
+
 }  // namespace
 
 std::unique_ptr<GraphProcess> make_negate(ComputeSession& s, std::string n) {
@@ -811,6 +892,8 @@ std::unique_ptr<GraphProcess> make_process(ComputeSession& s, std::string_view k
     if (kind == "rss_combine") return make_rss_combine(s, n);
     if (kind == "sens_recon") return make_sens_recon(s, n);
     if (kind == "rss_recon") return make_rss_recon(s, n);
+    if (kind == "sense_forward") return std::make_unique<SenseModelProcess>(s, n, false);
+    if (kind == "sense_normal") return std::make_unique<SenseModelProcess>(s, n, true);
     throw InvalidArgument("unknown process kind '" + std::string(kind) + "'");
 }
 

@@ -50,6 +50,7 @@ struct StridedArgs {
     int shift_out;  // fftshift along the axis on store
     float scale;
     const float2* tw;
+    const float* mask = nullptr;  // k-space sampling mask [nx, N] (forward-model kernels only)
 };
 
 enum class Combine : int { None = 0, Sense = 1, Rss = 2 };
@@ -95,5 +96,20 @@ cudaError_t launch_strided(std::uint64_t N, int dir, const StridedArgs& a, const
                            cudaStream_t stream);
 cudaError_t launch_contig(std::uint64_t N, int dir, Combine mode, const ContigArgs& a,
                           const LaunchShape& s, cudaStream_t stream);
+
+// ---- SENSE forward model E = P F S and normal operator E^H E ----
+
+// Expand + forward axis-0 FFT: out line (y, c, f) = F_x( S[:, y, c] * M[:, y, f] ).
+// a.in = M [N, ny, F], a.smap = S [N, ny, C], a.out = [N, ny, C, F].
+LaunchShape plan_expand(std::uint64_t N, std::uint64_t items /* ny*C*F */, int device_sms);
+cudaError_t launch_expand(std::uint64_t N, const ContigArgs& a, const LaunchShape& s, cudaStream_t stream);
+
+// Forward axis-1 FFT of every column with the sampling mask applied at the
+// store (roundtrip = false), or forward FFT, mask, inverse FFT in registers
+// (roundtrip = true: the k-space never leaves the SM).  a.mask may be null.
+// Square images only (a.nx == N).
+LaunchShape plan_strided_masked(std::uint64_t N, bool roundtrip, std::uint64_t planes, int device_sms);
+cudaError_t launch_strided_masked(std::uint64_t N, bool roundtrip, const StridedArgs& a, const LaunchShape& s,
+                                  cudaStream_t stream);
 
 }  // namespace hetreco::dev

@@ -153,3 +153,18 @@ def test_port_matches_reference_live():
     assert beq(o.rss_recon(Y), o.ref_recon("rss", Y)[0])
     x = rng.random(5000).astype(np.float32)
     assert beq(o.negate(x, 0.75), o.ref_run_kernel("negate", x, struct.pack("<d", 0.75), x.size))
+
+
+def test_sense_forward_oracle_vs_numpy():
+    rng = np.random.default_rng(31)
+    M = cplx(rng, 32, 32, 2)
+    S = cplx(rng, 32, 32, 3)
+    mask = (rng.random((32, 32)) < 0.4).astype(np.float32)
+    Y = o.sense_forward(M, S, mask)
+    ref = np.fft.fft2(S[..., None].astype(np.complex128) * M[:, :, None, :], axes=(0, 1)) * mask[:, :, None, None]
+    assert relmax(Y, ref) <= 1e-6
+    # adjoint identity <E m, y> == <m, E^H y> (E^H = nx*ny * sens_recon)
+    y = cplx(rng, 32, 32, 3, 2) * mask[:, :, None, None]
+    lhs = np.vdot(o.sense_forward(M, S, mask), y)
+    rhs = np.vdot(M, o.sens_recon(np.asfortranarray(y.astype(np.complex64)), S)) * 32 * 32
+    assert abs(lhs - rhs) <= 1e-4 * abs(lhs)
