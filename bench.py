@@ -298,19 +298,103 @@ def run_ours(args):
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(Y, S)
 
+    extras = None
+    if rank == 0 and not args.no_extras:
+        extras = other_configs(h, s, peak, args.c5_frames)
+
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": t_max / args.steps * 1e3, "higher_is_better": True,
-                "scaling": "weak", "vs_baseline": None, "dtype": "f32 (complex64 I/O, fp64 coil accumulation)",
+                "scaling": "weak", "vs_baseline": None, "dtype": "f32 (complex64 I/O, fp32 FFT and coil accumulation)",
                 "data": "synthetic (seeded N(0,1) k-space, normalised random sensitivity maps)",
                 "config": dict(CONFIG, parallelism=f"frame-slab x{world} (no collective)"),
                 "impl": "hetreco-b200",
                 "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu, "clocks": clocks,
-                "gpu_launches": 2 * args.steps}
+                "gpu_launches": 2 * args.steps, "other_configs": extras}
         print(json.dumps(line), flush=True)
     if world > 1:
         import torch.distributed as dist
         dist.destroy_process_group()
+
+
+def _device_time(s, fn, reps: int) -> float:
+    """Mean device seconds of fn() over reps (CUDA events on the compute stream)."""
+    for _ in range(3):
+        fn()
+    s.synchronize()
+    s.timer_start()
+    for _ in range(reps):
+        fn()
+    return s.timer_stop() / reps
+
+
+def other_configs(h, s, peak: float, c5_frames: int):
+    """Side measurements for BASELINE.json configs 0, 1, 3, 4 (the headline is
+    config 2 = C3).  All device-resident except C5, which streams from pinned
+    host memory like the e2e leg."""
+    rng = np.random.default_rng(99)
+    out = {}
+    # C1: Negate on one 512x512 float32 image (paper's minimal example)
+    x = np.asfortranarray(rng.random((512, 512), dtype=np.float32))
+    hx = s.register_data([x])
+    hy = s.allocate_data([((512, 512), np.float32)])
+    p = h.Process(s, "negate").set_input(hx).set_output(hy).init({"max_value": 1.0})
+    t = _device_time(s, p.launch, 200)
+    out["C1_negate_512x512_f32"] = {"us_per_image": t * 1e6, "images_per_s": 1 / t,
+                                    "gbs": 2 * x.nbytes / t / 1e9, "frac_of_hbm": 2 * x.nbytes / t / 1e9 / peak,
+                                    "note": "2 MB per image: launch-latency bound"}
+    # C2: single-frame 256x256, 8 coils, IFFT + RSS
+    Y2 = np.asfortranarray((rng.standard_normal((256, 256, 8, 1), dtype=np.float32)
+                            + 1j * rng.standard_normal((256, 256, 8, 1), dtype=np.float32)).astype(np.complex64))
+    hk = s.register_data(h.Data([Y2], h.DataKind.KData))
+    hr = s.allocate_data([((256, 256, 1), np.float32)], h.DataKind.XData)
+    p2 = h.Process(s, "rss_recon").set_input(hk).set_output(hr).init()
+    t2 = _device_time(s, p2.launch, 200)
+    out["C2_rss_256x256x8x1"] = {"us_per_frame": t2 * 1e6, "frames_per_s": 1 / t2,
+                                 "gbs": (Y2.nbytes + 256 * 256 * 4) / t2 / 1e9}
+    # C4: iterative loop -- normal operator E^H E (FFT + mask + IFFT + coil combine)
+    # on C2 shapes, launched 100x after one init()
+    S2 = np.asfortranarray((rng.standard_normal((256, 256, 8), dtype=np.float32) + 0j).astype(np.complex64))
+    M2 = np.asfortranarray(Y2[:, :, 0, :])
+    mask = np.asfortranarray((rng.random((256, 256)) < 0.33).astype(np.float32))
+    hn = s.register_data(h.Data([M2, S2, mask], h.DataKind.XData))
+    ho = s.allocate_data([((256, 256, 1), np.complex64)], h.DataKind.XData)
+    p4 = h.Process(s, "sense_normal").set_input(hn).set_output(ho).init()
+    s.synchronize()
+    t0 = time.perf_counter()
+    s.timer_start()
+    for _ in range(100):
+        p4.launch()
+    t4 = s.timer_stop() / 100
+    wall = (time.perf_counter() - t0) / 100
+    st = p4.stats()
+    out["C4_normal_op_256x256x8_x100"] = {
+        "us_per_launch_device": t4 * 1e6, "us_per_launch_wall": wall * 1e6, "launches": st.launches,
+        "init_calls": st.init_calls, "init_ms": st.init_seconds * 1e3,
+        "kernels_per_launch": 3, "note": "one cudaGraphLaunch per launch(); plans/twiddles baked in init()"}
+    # C5: 512x512x32 coils streamed from pinned host memory (RSS), per GPU slab
+    if c5_frames > 0:
+        Y5 = h.pinned_empty((512, 512, 32, c5_frames), np.complex64)
+        for f in range(c5_frames):
+            Y5[..., f] = (rng.standard_normal((512, 512, 32), dtype=np.float32)
+                          + 1j * rng.standard_normal((512, 512, 32), dtype=np.float32))
+        R5 = h.pinned_empty((512, 512, c5_frames), np.float32)
+        st5 = h.StreamingRecon(s, "rss", 512, 512, 32, 2)
+        st5.run(Y5, R5)
+        t0 = time.perf_counter()
+        for _ in range(3):
+            st5.run(Y5, R5)
+        t5 = (time.perf_counter() - t0) / 3
+        out["C5_stream_rss_512x512x32"] = {"frames_per_gpu": c5_frames, "frames_per_s": c5_frames / t5,
+                                           "host_link_gbs": Y5.nbytes / t5 / 1e9,
+                                           "note": "pinned H2D of 64 MiB/frame dominates (PCIe)"}
+        hk5 = s.register_data(h.Data([np.asfortranarray(Y5[..., :2])], h.DataKind.KData))
+        hr5 = s.allocate_data([((512, 512, 2), np.float32)], h.DataKind.XData)
+        p5 = h.Process(s, "rss_recon").set_input(hk5).set_output(hr5).init()
+        t5d = _device_time(s, p5.launch, 20)
+        out["C5_stream_rss_512x512x32"]["device_frames_per_s"] = 2 / t5d
+        out["C5_stream_rss_512x512x32"]["device_gbs"] = 2 * (512 * 512 * 32 * 8 + 512 * 512 * 4) / t5d / 1e9
+    return out
 
 
 def main():
@@ -322,6 +406,8 @@ def main():
     ap.add_argument("--chunk", type=int, default=6, help="frames per streamed chunk (e2e)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extras", action="store_true", help="skip the C1/C2/C4/C5 side measurements")
+    ap.add_argument("--c5-frames", type=int, default=8, help="frames of the C5 512^2x32 streamed slab")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
