@@ -692,11 +692,15 @@ public:
     ReconProcess(ComputeSession& s, std::string name, dev::Combine mode)
         : GraphProcess(s, std::move(name)), mode_(mode) {}
     void bake(const ProcessParams& p) override {
-        p.require_known({"shift", "chunk_frames", "accumulate", "prefetch"});
+        p.require_known({"shift", "chunk_frames", "accumulate", "prefetch", "algorithm", "max_clusters", "cluster_size"});
         shift_ = p.get_bool("shift", false);
         const std::string acc = p.get_string("accumulate", "fp32");
         if (acc != "fp32" && acc != "fp64")
             throw InvalidParams(name() + ": accumulate must be \"fp32\" or \"fp64\"");
+        std::string algo = p.get_string("algorithm", "auto");
+        if (algo != "auto" && algo != "cluster" && algo != "two_pass")
+            throw InvalidParams(name() + ": algorithm must be \"auto\", \"cluster\" or \"two_pass\"");
+        if (const char* v = std::getenv("HETRECO_RECON_ALGO"); v && *v && algo == "auto") algo = v;
         variant_ = (acc == "fp32" ? 1 : 0) | (p.get_bool("prefetch", true) ? 2 : 0);
         if (const char* v = std::getenv("HETRECO_COMBINE_VARIANT")) variant_ = std::atoi(v);
         const LayoutDescriptor& li = input_layout();
@@ -723,6 +727,39 @@ public:
         }
         y_ = static_cast<const float2*>(session().device_array(require_input(), 0));
         out_ = session().device_array(require_output(), 0);
+        const int ord = session().cuda().ordinal();
+        // Single-pass cluster kernel (fft_cluster.cu), 256x256 with fp32
+        // accumulation, on request.  "auto" keeps the two-pass chain: measured
+        // faster on B200 (profiles/round1_cluster.md -- the cluster kernel
+        // reaches only 120 of 148 SMs and is bound by per-SM shared-memory
+        // traffic, not HBM).
+        cluster_ = false;
+        if (algo == "cluster") {
+            const bool ok = dev::cluster_supported(nx_, ny_, mode_) && acc == "fp32";
+            if (!ok && algo == "cluster")
+                throw InvalidParams(name() + ": algorithm \"cluster\" needs 256x256 images and fp32 accumulation, got " +
+                                    dims_str(y) + " / " + acc);
+            if (ok) {
+                const std::int64_t mc = p.get_int("max_clusters", 0);
+                if (mc < 0) throw InvalidParams(name() + ": max_clusters must be >= 0");
+                const std::int64_t cs = p.get_int("cluster_size", 0);
+                if (cs != 0 && cs != 8 && cs != 16) throw InvalidParams(name() + ": cluster_size must be 8 or 16");
+                cplan_ = dev::plan_cluster(mode_, nc_, nf_, int(mc), int(cs));
+                if (cplan_.clusters <= 0) {
+                    if (algo == "cluster") throw DeviceError(name(), "cluster kernel does not fit on this device");
+                } else {
+                    cluster_ = true;
+                    if (cws_.size() != cplan_.ws_bytes) cws_ = DevMem(cplan_.ws_bytes);
+                    ccnt_ = DevMem(cplan_.cnt_bytes);
+                    ck(cudaMemset(ccnt_.get(), 0, cplan_.cnt_bytes), "cudaMemset(cluster counters)");
+                    ck(cudaDeviceSynchronize(), "cluster counters");
+                    ctw_ = twiddle_table(nx_, +1);
+                    ck(dev::make_cluster_map(cmap_, y_, ny_ * nc_ * nf_, cplan_.cl), name() + ": TMA descriptor");
+                    scratch_ = DevMem();
+                    return;
+                }
+            }
+        }
         // Frames may be processed in chunks to bound the axis-1 intermediate
         // (scratch = chunk_frames * nx*ny*coils*8 bytes).  Default: one chunk
         // of all frames -- measured fastest on B200, because the combine pass
@@ -735,7 +772,6 @@ public:
         chunk_ = std::min<std::uint64_t>(std::uint64_t(chunk), nf_);
         const std::uint64_t scratch_bytes = frame_bytes * chunk_;
         if (scratch_.size() != scratch_bytes) scratch_ = DevMem(scratch_bytes);
-        const int ord = session().cuda().ordinal();
         plan_.make(nx_, ny_, +1, nc_ * chunk_, mode_, ny_ * chunk_, ord);
         // prefetch form measured per size on B200: register copy at 256,
         // ping-pong (two-way unrolled) at 512 (profiles/round1_summary.md)
@@ -749,6 +785,13 @@ public:
     }
     void record(cudaStream_t s) override {
         const float scale = float(1.0 / (double(nx_) * double(ny_)));
+        if (cluster_) {
+            dev::ClusterLaunch a{smap_, out_, cws_.as<float2>(), ccnt_.as<unsigned>(), ctw_.as<float2>(), nc_, nf_,
+                                 shift_, scale};
+            ck(dev::launch_cluster(mode_, cmap_, a, cplan_, s), name() + "/cluster ifft2+combine");
+            mark(s);
+            return;
+        }
         const std::uint64_t plane = nx_ * ny_;
         const std::uint64_t out_elem = mode_ == dev::Combine::Sense ? 8 : 4;
         for (std::uint64_t f0 = 0; f0 < nf_; f0 += chunk_) {
@@ -776,6 +819,10 @@ private:
     DevMem scratch_;
     FftPlan plan_;
     dev::LaunchShape tail_s1_, tail_s2_;
+    bool cluster_ = false;
+    dev::ClusterPlan cplan_;
+    dev::ClusterMap cmap_{};
+    DevMem cws_, ccnt_, ctw_;
 };
 
 // SENSE forward model E m = P F (S m) ("sense_forward") and the normal

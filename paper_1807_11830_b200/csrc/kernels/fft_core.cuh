@@ -218,6 +218,28 @@ struct LineFFT {
     template <int DIR, class Sync>
     __device__ __forceinline__ static void run(float2 (&v)[R], const float2 (&tw)[NTW], float2* line, int j,
                                                Sync&& sync, float scale = 1.0f) {
+        run_f<DIR>(
+            v,
+            [&](auto pc, auto sc, auto qc) {
+                return tw[tw_offset(pc.value) + sc.value * (radix(pc.value) - 1) + qc.value];
+            },
+            line, j, sync, scale);
+    }
+
+    // Twiddle for pass p (>= 1), sub-group s, q = qc + 1 of thread j from a
+    // W_N^t table (shared or global): table[(g mod Ns) * q * N/(Ns*Rp)].
+    template <int p, int s, int qc>
+    __device__ __forceinline__ static int tw_index(int j) {
+        constexpr int Rp = radix(p), Ns = ns(p), stride = N / (Ns * Rp);
+        return ((j + s * T) % Ns) * (qc + 1) * stride;
+    }
+
+    // As run(), with the pass twiddles supplied by `twf(pass, s, qc)` (all
+    // three std::integral_constant) -- e.g. read from a shared-memory table
+    // at the point of use instead of held in registers.
+    template <int DIR, class TwF, class Sync>
+    __device__ __forceinline__ static void run_f(float2 (&v)[R], TwF&& twf, float2* line, int j, Sync&& sync,
+                                                 float scale = 1.0f) {
         sfor<P>([&](auto pc) {
             constexpr int p = pc.value;
             constexpr int Rp = radix(p), Ns = ns(p), S = R / Rp;
@@ -236,7 +258,7 @@ struct LineFFT {
                 sfor<S>([&](auto sc) {
                     sfor<Rp - 1>([&](auto qc) {
                         constexpr int m = sc.value + (qc.value + 1) * S;
-                        v[m] = cmul(v[m], tw[tw_offset(p) + sc.value * (Rp - 1) + qc.value]);
+                        v[m] = cmul(v[m], twf(pc, sc, qc));
                     });
                 });
             }

@@ -97,6 +97,48 @@ cudaError_t launch_strided(std::uint64_t N, int dir, const StridedArgs& a, const
 cudaError_t launch_contig(std::uint64_t N, int dir, Combine mode, const ContigArgs& a,
                           const LaunchShape& s, cudaStream_t stream);
 
+// ---- single-pass cluster reconstruction (fft_cluster.cu) ------------------------
+//
+// IFFT2 + Sense/Rss combine of [256, 256, C, F] k-space in ONE kernel: an
+// 8-CTA cluster holds a coil image across its SMs (TMA tile loads, DSMEM
+// transpose), coils accumulate in registers.  fp32 accumulation only.
+
+bool cluster_supported(std::uint64_t nx, std::uint64_t ny, Combine mode);
+int cluster_smem_bytes(int cluster_size);
+
+struct ClusterPlan {
+    int cl = 0;                   // CTAs per cluster (8 or 16)
+    int clusters = 0;             // resident clusters launched (persistent grid)
+    std::uint64_t ws_bytes = 0;   // split-frame partials workspace
+    std::uint64_t cnt_bytes = 0;  // split-frame arrival counters (zero-initialise once)
+};
+// max_clusters <= 0: as many as fit on the device; cluster_size 0 = pick
+// (HETRECO_CLUSTER_SIZE, else 16 when it launches, else 8).  clusters == 0
+// in the result: the kernel cannot run here.
+ClusterPlan plan_cluster(Combine mode, std::uint64_t coils, std::uint64_t frames, int max_clusters = 0,
+                         int cluster_size = 0);
+
+// Opaque TMA descriptor (CUtensorMap) for the k-space array [256, rows]
+// (rows = 256 * C * F), box = one CTA's column tile for cluster size `cl`;
+// re-made when the k-space pointer changes.
+struct alignas(64) ClusterMap {
+    unsigned char bytes[128];
+};
+cudaError_t make_cluster_map(ClusterMap& m, const float2* y, std::uint64_t rows, int cl);
+
+struct ClusterLaunch {
+    const float2* smap;  // Sense: S [256, 256, C]
+    void* out;           // [256, 256, F]
+    float2* ws;
+    unsigned* cnt;
+    const float2* tw;  // inverse W_256^t table
+    std::uint64_t coils, frames;
+    int shift;
+    float scale;
+};
+cudaError_t launch_cluster(Combine mode, const ClusterMap& m, const ClusterLaunch& a, const ClusterPlan& p,
+                           cudaStream_t st);
+
 // ---- SENSE forward model E = P F S and normal operator E^H E ----
 
 // Expand + forward axis-0 FFT: out line (y, c, f) = F_x( S[:, y, c] * M[:, y, f] ).

@@ -39,6 +39,7 @@ for _ in range(a.launches):
 s.synchronize()
 if a.reps:
     t = p.profile(a.reps)
+    if len(t) % 2: t = t + [0.0]
     t1, t2 = sum(t[0::2]), sum(t[1::2])
     fy = nx * ny * a.coils * 8
     b1 = 2 * fy * a.frames
@@ -49,5 +50,5 @@ if a.reps:
     tg = s.timer_stop() / a.timed
     print(f"{a.method} {nx}x{ny}x{a.coils}x{a.frames} variant={os.environ.get('HETRECO_COMBINE_VARIANT', '-')} "
           f"chunk={os.environ.get('HETRECO_CHUNK', 'auto')} kernels={len(t)} | axis1 {t1*1e6:.1f} us {b1/t1/1e9:.0f} GB/s "
-          f"| axis0+combine {t2*1e6:.1f} us {b2/t2/1e9:.0f} GB/s | sum {(t1+t2)*1e6:.1f} us | graph {tg*1e6:.1f} us "
+          f"| axis0+combine {t2*1e6:.1f} us {b2/max(t2, 1e-12)/1e9:.0f} GB/s | sum {(t1+t2)*1e6:.1f} us | graph {tg*1e6:.1f} us "
           f"= {a.frames/tg:.0f} frames/s")

@@ -490,3 +490,77 @@ def test_c3_full_size_properties(s):
     p.launch()
     M2 = s.fetch_data(hout).arrays[0]
     assert relmax(M2, 2.5 * M) <= TOL
+
+
+# ---- single-pass cluster kernel (algorithm="cluster", fft_cluster.cu) -------------------
+
+@pytest.mark.parametrize("cluster_size", [8, 16])
+@pytest.mark.parametrize("method", ["sens_recon", "rss_recon"])
+@pytest.mark.parametrize("nc,nf,max_clusters,shift", [(6, 5, 0, False), (5, 3, 7, False), (4, 3, 5, True),
+                                                       (3, 2, 1, True), (7, 1, 3, False)],
+                         ids=lambda v: str(v))
+def test_cluster_recon_vs_oracle(s, method, cluster_size, nc, nf, max_clusters, shift):
+    """TMA tile loads + DSMEM transpose + register coil accumulation, including
+    frames split across clusters (max_clusters not dividing frames*coils: the
+    last-arriving piece adds the partial sums)."""
+    rng = np.random.default_rng(100 + nc * 10 + nf)
+    Y = cplx(rng, 256, 256, nc, nf)
+    S = cplx(rng, 256, 256, nc)
+    prm = {"algorithm": "cluster", "cluster_size": cluster_size, "max_clusters": max_clusters, "shift": shift}
+    ax = (0, 1)
+    Yo = np.asfortranarray(np.fft.ifftshift(Y, axes=ax)) if shift else Y
+    if method == "sens_recon":
+        So = np.asfortranarray(np.fft.ifftshift(S, axes=ax)) if shift else S
+        ref = o.sens_recon(Yo, So)
+        (M,), p = run_process(s, method, [Y, S], [((256, 256, nf), np.complex64)], prm)
+    else:
+        ref = o.rss_recon(Yo)
+        (M,), p = run_process(s, method, [Y], [((256, 256, nf), np.float32)], prm)
+    if shift:
+        ref = np.fft.fftshift(ref, axes=ax)
+    assert relmax(M, ref) <= TOL
+
+
+def test_cluster_recon_relaunch_and_two_pass_agreement(s):
+    """Counters self-reset: repeated launches give identical results; with
+    whole frames per cluster the result is bit-identical to the two-pass chain
+    (same per-coil arithmetic, same coil order)."""
+    nx, nc, nf = 256, 4, 6
+    rng = np.random.default_rng(5)
+    Y = cplx(rng, nx, nx, nc, nf)
+    S = cplx(rng, nx, nx, nc)
+    hin = s.register_data(h.Data([Y, S], h.DataKind.KData))
+    outs = []
+    for prm in ({"algorithm": "cluster", "max_clusters": 5},        # frames split across clusters
+                {"algorithm": "cluster", "max_clusters": nf},       # one frame per cluster
+                {"algorithm": "two_pass"}):
+        hout = s.allocate_data([((nx, nx, nf), np.complex64)])
+        p = h.Process(s, "sens_recon").set_input(hin).set_output(hout).init(prm)
+        p.launch()
+        first = s.fetch_data(hout).arrays[0]
+        for _ in range(3):
+            p.launch()
+        again = s.fetch_data(hout).arrays[0]
+        assert np.array_equal(first, again)
+        outs.append(first)
+    assert relmax(outs[0], outs[2]) <= TOL
+    assert np.array_equal(outs[1], outs[2])
+
+
+def test_cluster_recon_rejects_unsupported(s):
+    rng = np.random.default_rng(6)
+    Y = cplx(rng, 128, 128, 2, 1)
+    S = cplx(rng, 128, 128, 2)
+    hin = s.register_data(h.Data([Y, S], h.DataKind.KData))
+    hout = s.allocate_data([((128, 128, 1), np.complex64)])
+    with pytest.raises(h.InvalidParams):
+        h.Process(s, "sens_recon").set_input(hin).set_output(hout).init({"algorithm": "cluster"})
+    Y2 = cplx(rng, 256, 256, 2, 1)
+    hin2 = s.register_data(h.Data([Y2, cplx(rng, 256, 256, 2)], h.DataKind.KData))
+    hout2 = s.allocate_data([((256, 256, 1), np.complex64)])
+    with pytest.raises(h.InvalidParams):
+        h.Process(s, "sens_recon").set_input(hin2).set_output(hout2).init({"algorithm": "cluster", "accumulate": "fp64"})
+    with pytest.raises(h.InvalidParams):
+        h.Process(s, "sens_recon").set_input(hin2).set_output(hout2).init({"algorithm": "cluster", "cluster_size": 4})
+    with pytest.raises(h.InvalidParams):
+        h.Process(s, "sens_recon").set_input(hin2).set_output(hout2).init({"algorithm": "fastest"})
