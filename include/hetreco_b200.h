@@ -215,6 +215,32 @@ int hetreco_parse_layout_header(const void* bytes, uint64_t nbytes, hetreco_arra
 /* DeviceFilter::parse + describe (device.hpp:76-86) */
 int hetreco_filter_describe(const char* filter_text, char* buf, uint64_t cap);
 
+/* ---- io: MAT v5 / PGM-PPM / raw+sidecar (SPEC.md io module :470-533) ----
+ * Readers return a variable list; payloads stay owned by it (and are
+ * page-locked when pinned != 0, ready for register_data / hetreco_stream_run
+ * DMA) until hetreco_mat_free.  Error codes 22..26: MalformedFile,
+ * UnsupportedFeature (message names the feature), IoError, SizeMismatch,
+ * MalformedSidecar. */
+typedef struct hetreco_mat_t* hetreco_mat;
+/* read_mat(path) */
+int hetreco_mat_read(const char* path, int pinned, hetreco_mat* out);
+/* the same parser over an in-memory file image */
+int hetreco_mat_parse(const void* bytes, uint64_t size, int pinned, hetreco_mat* out);
+/* read_image: one variable "image", UINT8 [w,h] (P5) or [3,w,h] (P6) */
+int hetreco_image_read(const char* path, int pinned, hetreco_mat* out);
+/* read_raw: one variable "raw" */
+int hetreco_raw_read(const char* path, const char* sidecar_path, int pinned, hetreco_mat* out);
+int hetreco_mat_count(hetreco_mat m, int* count);
+/* variable `index`: name (NUL-terminated into name[cap]) and desc (type, rank,
+ * dims, host = payload pointer, offset_bytes = 1 when page-locked) */
+int hetreco_mat_variable(hetreco_mat m, int index, char* name, uint64_t cap, hetreco_array_desc* desc);
+int hetreco_mat_free(hetreco_mat m);
+/* write_mat(path, variables); arrays[i].host = payload */
+int hetreco_mat_write(const char* path, int count, const char* const* names, const hetreco_array_desc* arrays);
+/* write_image (UINT8, or FLOAT32 in [0,1] -> round(v*255)) */
+int hetreco_image_write(const char* path, const hetreco_array_desc* image);
+int hetreco_raw_write(const char* path, const char* sidecar_path, const hetreco_array_desc* array);
+
 #if defined(__GNUC__)
 #pragma GCC visibility pop
 #endif

@@ -36,6 +36,12 @@ enum class ErrorCode : int {
     ChainMismatch,
     ChainStageError,
     UnsupportedElementType,
+    // io (SPEC.md io module)
+    MalformedFile,
+    UnsupportedFeature,
+    IoError,
+    SizeMismatch,
+    MalformedSidecar,
 };
 
 class Error : public std::runtime_error {
@@ -71,6 +77,11 @@ HETRECO_SIMPLE_ERROR(AlreadyInitialized);     // errors.hpp:147
 HETRECO_SIMPLE_ERROR(NotInitialized);         // errors.hpp:152
 HETRECO_SIMPLE_ERROR(ChainMismatch);          // errors.hpp:158
 HETRECO_SIMPLE_ERROR(UnsupportedElementType); // errors.hpp:179
+HETRECO_SIMPLE_ERROR(MalformedFile);          // SPEC.md:494 (io)
+HETRECO_SIMPLE_ERROR(UnsupportedFeature);     // message names the feature
+HETRECO_SIMPLE_ERROR(IoError);
+HETRECO_SIMPLE_ERROR(SizeMismatch);
+HETRECO_SIMPLE_ERROR(MalformedSidecar);
 #undef HETRECO_SIMPLE_ERROR
 
 // A kernel failed on the device; names the kernel (errors.hpp:73-83).

@@ -10,6 +10,7 @@
 #include <string>
 
 #include "../kernels/launch.hpp"
+#include "hetreco_b200/io.hpp"
 #include "hetreco_b200/processes.hpp"
 
 using namespace hetreco;
@@ -38,6 +39,9 @@ struct hetreco_stream_t {
 };
 struct hetreco_cuda_backend_t {
     std::unique_ptr<CudaBackend> b;
+};
+struct hetreco_mat_t {
+    std::vector<io::MatVariable> vars;
 };
 
 namespace {
@@ -625,6 +629,127 @@ int hetreco_parse_layout_header(const void* bytes, uint64_t n, hetreco_array_des
             for (int d = 0; d < 8; ++d) out[i].dims[d] = l.records[i].dims[d];
             out[i].offset_bytes = l.records[i].offset_bytes;
         }
+    });
+}
+
+}  // extern "C"
+
+// ---- io (SPEC.md io module :470-533; include/hetreco_b200/io.hpp) --------------------
+
+namespace {
+NDArray array_of_desc(const hetreco_array_desc& d) {
+    ArrayShape sh = shape_of(d);
+    NDArray a(sh.element_type, sh.dims);
+    if (a.byte_size()) {
+        need(d.host, "array payload");
+        std::memcpy(a.bytes().data(), d.host, a.byte_size());
+    }
+    return a;
+}
+HostMemory mem_of(int pinned) { return pinned ? HostMemory::Pinned : HostMemory::Pageable; }
+}  // namespace
+
+extern "C" {
+
+int hetreco_mat_read(const char* path, int pinned, hetreco_mat* out) {
+    return guard([&] {
+        need(path, "path");
+        need(out, "out");
+        auto m = std::make_unique<hetreco_mat_t>();
+        m->vars = io::read_mat(path, mem_of(pinned));
+        *out = m.release();
+    });
+}
+
+int hetreco_mat_parse(const void* bytes, uint64_t size, int pinned, hetreco_mat* out) {
+    return guard([&] {
+        need(bytes, "bytes");
+        need(out, "out");
+        auto m = std::make_unique<hetreco_mat_t>();
+        m->vars = io::parse_mat(static_cast<const std::byte*>(bytes), size, mem_of(pinned));
+        *out = m.release();
+    });
+}
+
+int hetreco_image_read(const char* path, int pinned, hetreco_mat* out) {
+    return guard([&] {
+        need(path, "path");
+        need(out, "out");
+        auto m = std::make_unique<hetreco_mat_t>();
+        m->vars.push_back({"image", io::read_image(path, mem_of(pinned))});
+        *out = m.release();
+    });
+}
+
+int hetreco_raw_read(const char* path, const char* sidecar_path, int pinned, hetreco_mat* out) {
+    return guard([&] {
+        need(path, "path");
+        need(sidecar_path, "sidecar_path");
+        need(out, "out");
+        auto m = std::make_unique<hetreco_mat_t>();
+        m->vars.push_back({"raw", io::read_raw(path, sidecar_path, mem_of(pinned))});
+        *out = m.release();
+    });
+}
+
+int hetreco_mat_count(hetreco_mat m, int* count) {
+    return guard([&] {
+        need(m, "mat");
+        need(count, "count");
+        *count = int(m->vars.size());
+    });
+}
+
+int hetreco_mat_variable(hetreco_mat m, int index, char* name, uint64_t cap, hetreco_array_desc* desc) {
+    return guard([&] {
+        need(m, "mat");
+        need(desc, "desc");
+        if (index < 0 || std::size_t(index) >= m->vars.size())
+            throw InvalidArgument("variable index " + std::to_string(index) + " out of range");
+        io::MatVariable& v = m->vars[std::size_t(index)];
+        if (name && cap) copy_str(name, cap, v.name);
+        std::memset(desc, 0, sizeof *desc);
+        desc->element_type = std::uint64_t(v.array.element_type());
+        desc->rank = std::uint32_t(v.array.rank());
+        for (std::size_t i = 0; i < v.array.rank(); ++i) desc->dims[i] = v.array.dims()[i];
+        desc->host = v.array.bytes().data();
+        desc->offset_bytes = v.array.pinned() ? 1 : 0;  // io: 1 = payload is page-locked
+    });
+}
+
+int hetreco_mat_free(hetreco_mat m) {
+    return guard([&] { delete m; });
+}
+
+int hetreco_mat_write(const char* path, int count, const char* const* names, const hetreco_array_desc* arrays) {
+    return guard([&] {
+        need(path, "path");
+        if (count < 0) throw InvalidArgument("count must be >= 0");
+        std::vector<io::MatVariable> vars;
+        for (int i = 0; i < count; ++i) {
+            need(names, "names");
+            need(arrays, "arrays");
+            need(names[i], "variable name");
+            vars.push_back({names[i], array_of_desc(arrays[i])});
+        }
+        io::write_mat(path, vars);
+    });
+}
+
+int hetreco_image_write(const char* path, const hetreco_array_desc* image) {
+    return guard([&] {
+        need(path, "path");
+        need(image, "image");
+        io::write_image(path, array_of_desc(*image));
+    });
+}
+
+int hetreco_raw_write(const char* path, const char* sidecar_path, const hetreco_array_desc* array) {
+    return guard([&] {
+        need(path, "path");
+        need(sidecar_path, "sidecar_path");
+        need(array, "array");
+        io::write_raw(path, sidecar_path, array_of_desc(*array));
     });
 }
 

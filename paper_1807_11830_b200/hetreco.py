@@ -35,7 +35,8 @@ _ERROR_NAMES = ["Ok", "Error", "InvalidFilter", "NoMatchingDevice", "InvalidArgu
                 "MalformedHeader", "AllocationFailure", "UnknownHandle", "DeviceError", "CompileError",
                 "DuplicateKernel", "UnsupportedSource", "UnknownKernel", "InvalidParams", "ShapeMismatch",
                 "AlreadyInitialized", "NotInitialized", "ChainMismatch", "ChainStageError",
-                "UnsupportedElementType"]
+                "UnsupportedElementType", "MalformedFile", "UnsupportedFeature", "IoError", "SizeMismatch",
+                "MalformedSidecar"]
 ERRORS: dict[int, type] = {1: HetrecoError}
 for _code, _name in enumerate(_ERROR_NAMES):
     if _code >= 2:
@@ -84,6 +85,8 @@ EXPORTED = [
     "hetreco_stream_create", "hetreco_stream_run", "hetreco_stream_destroy", "hetreco_pack_layout",
     "hetreco_parse_layout_header", "hetreco_filter_describe", "hetreco_process_profile",
     "hetreco_session_timer_start", "hetreco_session_timer_stop",
+    "hetreco_mat_read", "hetreco_mat_parse", "hetreco_image_read", "hetreco_raw_read", "hetreco_mat_count",
+    "hetreco_mat_variable", "hetreco_mat_free", "hetreco_mat_write", "hetreco_image_write", "hetreco_raw_write",
 ]
 
 
@@ -137,6 +140,13 @@ def lib():
         "hetreco_pack_layout": ([i32, vp, u64, vp, u64, vp], i32),
         "hetreco_parse_layout_header": ([vp, u64, vp, i32, vp, vp, vp], i32),
     }
+    sig.update({
+        "hetreco_mat_read": ([pc, i32, vp], i32), "hetreco_mat_parse": ([vp, u64, i32, vp], i32),
+        "hetreco_image_read": ([pc, i32, vp], i32), "hetreco_raw_read": ([pc, pc, i32, vp], i32),
+        "hetreco_mat_count": ([vp, vp], i32), "hetreco_mat_variable": ([vp, i32, vp, u64, vp], i32),
+        "hetreco_mat_free": ([vp], i32), "hetreco_mat_write": ([pc, i32, vp, vp], i32),
+        "hetreco_image_write": ([pc, vp], i32), "hetreco_raw_write": ([pc, pc, vp], i32),
+    })
     for name, (args, res) in sig.items():
         f = getattr(L, name)
         f.argtypes = args
@@ -755,3 +765,76 @@ class CudaBackend:
 
 def version() -> str:
     return lib().hetreco_version().decode()
+
+
+# ---------------------------------------------------------------------------
+# io: MAT v5 / PGM-PPM / raw+sidecar (SPEC.md io module; include/hetreco_b200/io.hpp)
+# ---------------------------------------------------------------------------
+
+
+def _take_vars(m) -> list:
+    """Copies the variables of a native list into Fortran-ordered numpy arrays."""
+    L = lib()
+    try:
+        n = C.c_int()
+        _ck(L.hetreco_mat_count(m, C.byref(n)))
+        out = []
+        for i in range(n.value):
+            d = _ArrayDesc()
+            name = C.create_string_buffer(256)
+            _ck(L.hetreco_mat_variable(m, i, name, 256, C.byref(d)))
+            shape = tuple(int(d.dims[k]) for k in range(d.rank))
+            dt = np.dtype(dtype_of(d.element_type))
+            nbytes = int(np.prod(shape)) * dt.itemsize
+            buf = (C.c_char * nbytes).from_address(d.host)
+            a = np.frombuffer(buf, dtype=dt).reshape(shape, order="F").copy(order="F")
+            out.append((name.value.decode(errors="replace"), a))
+        return out
+    finally:
+        L.hetreco_mat_free(m)
+
+
+def read_mat(path: str) -> dict:
+    """read_mat: {name: array} in file order."""
+    m = C.c_void_p()
+    _ck(lib().hetreco_mat_read(os.fsencode(path), 0, C.byref(m)))
+    return dict(_take_vars(m))
+
+
+def parse_mat(data: bytes) -> dict:
+    m = C.c_void_p()
+    buf = C.create_string_buffer(bytes(data), len(data))
+    _ck(lib().hetreco_mat_parse(buf, len(data), 0, C.byref(m)))
+    return dict(_take_vars(m))
+
+
+def write_mat(path: str, variables) -> None:
+    """write_mat (SPEC.md:495-498); variables = {name: array} or [(name, array)]."""
+    items = list(variables.items()) if isinstance(variables, dict) else list(variables)
+    arrays = [np.asfortranarray(a) for _, a in items]
+    names = (C.c_char_p * max(1, len(items)))(*[str(n).encode() for n, _ in items])
+    _ck(lib().hetreco_mat_write(os.fsencode(path), len(items), names, _descs(arrays)))
+
+
+def read_image(path: str) -> np.ndarray:
+    """PGM (P5) -> uint8 [w, h]; PPM (P6) -> uint8 [3, w, h] (SPEC.md:499-505)."""
+    m = C.c_void_p()
+    _ck(lib().hetreco_image_read(os.fsencode(path), 0, C.byref(m)))
+    return _take_vars(m)[0][1]
+
+
+def write_image(path: str, image: np.ndarray) -> None:
+    a = np.asfortranarray(image)
+    _ck(lib().hetreco_image_write(os.fsencode(path), C.byref(_desc(a.shape, a.dtype, a.ctypes.data))))
+
+
+def read_raw(path: str, sidecar_path: str) -> np.ndarray:
+    m = C.c_void_p()
+    _ck(lib().hetreco_raw_read(os.fsencode(path), os.fsencode(sidecar_path), 0, C.byref(m)))
+    return _take_vars(m)[0][1]
+
+
+def write_raw(path: str, sidecar_path: str, array: np.ndarray) -> None:
+    a = np.asfortranarray(array)
+    _ck(lib().hetreco_raw_write(os.fsencode(path), os.fsencode(sidecar_path),
+                                C.byref(_desc(a.shape, a.dtype, a.ctypes.data))))
