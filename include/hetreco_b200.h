@@ -241,6 +241,17 @@ int hetreco_mat_write(const char* path, int count, const char* const* names, con
 int hetreco_image_write(const char* path, const hetreco_array_desc* image);
 int hetreco_raw_write(const char* path, const char* sidecar_path, const hetreco_array_desc* array);
 
+/* ---- gen_phantom ----------------------------
+ * Seeded synthetic cine on the session's device: truth = 3 rotating Gaussian
+ * blobs, smaps = normalised complex coil maps (sum |S|^2 = 1), kdata =
+ * F(S . truth).  Host outputs (COMPLEX64, column-major) may be NULL:
+ * kdata [nx,ny,coils,frames], smaps [nx,ny,coils], truth [nx,ny,frames].
+ * InvalidParams unless nx, ny are powers of two in [2, 4096]. */
+int hetreco_gen_phantom(hetreco_session s, uint64_t nx, uint64_t ny, uint64_t frames, uint64_t coils,
+                        uint64_t seed, void* kdata, void* smaps, void* truth);
+/* the seeded blob parameters (amp, radius, angle, sigma) x 3 -- host only */
+int hetreco_phantom_blobs(uint64_t nx, uint64_t ny, uint64_t seed, double* out12);
+
 #if defined(__GNUC__)
 #pragma GCC visibility pop
 #endif

@@ -276,6 +276,74 @@ def sense_normal(M, S, mask=None) -> np.ndarray:
     return sens_recon(sense_forward(M, S, mask), S)
 
 
+def phantom_blobs(nx: int, ny: int, seed: int):
+    """Blob parameters (amp, radius, angle, sigma) x 3 drawn from mt19937_64(seed)
+    with 53-bit uniforms -- restates hetreco::phantom_blobs (phantom.cpp), the
+    rule SPEC.md:452 leaves open ("centers/widths drawn from seeded generator")."""
+    mt = _MT19937_64(seed)
+    L = float(min(nx, ny))
+    out = []
+    for _ in range(3):
+        u = [float(mt.next() >> 11) * (1.0 / 9007199254740992.0) for _ in range(4)]
+        out.append((0.5 + 0.5 * u[0], 0.25 * L * u[1], 6.283185307179586 * u[2], L * (0.04 + 0.08 * u[3])))
+    return out
+
+
+class _MT19937_64:
+    """The standard 64-bit Mersenne Twister (std::mt19937_64), scalar Python."""
+
+    def __init__(self, seed: int):
+        self.mt = [0] * 312
+        self.mt[0] = seed & 0xFFFFFFFFFFFFFFFF
+        for i in range(1, 312):
+            self.mt[i] = (6364136223846793005 * (self.mt[i - 1] ^ (self.mt[i - 1] >> 62)) + i) & 0xFFFFFFFFFFFFFFFF
+        self.i = 312
+
+    def next(self) -> int:
+        M = 0xFFFFFFFFFFFFFFFF
+        if self.i >= 312:
+            for k in range(312):
+                x = (self.mt[k] & 0xFFFFFFFF80000000) | (self.mt[(k + 1) % 312] & 0x7FFFFFFF)
+                xa = x >> 1
+                if x & 1:
+                    xa ^= 0xB5026F5AA96619E9
+                self.mt[k] = self.mt[(k + 156) % 312] ^ xa
+            self.i = 0
+        y = self.mt[self.i]
+        self.i += 1
+        y ^= (y >> 29) & 0x5555555555555555
+        y ^= (y << 17) & 0x71D67FFFEDA60000
+        y ^= (y << 37) & 0xFFF7EEE000000000
+        y ^= y >> 43
+        return y & M
+
+
+def gen_phantom(nx: int, ny: int, frames: int, coils: int, seed: int):
+    """CPU port of gen_phantom (phantom.cu formulas) in fp64,
+    rounded once to complex64; Y = sense_forward(M_true, S) (the restated
+    forward FFT).  Returns (Y, S, M_true)."""
+    blobs = phantom_blobs(nx, ny, seed)
+    u = (np.arange(nx, dtype=np.float64) - 0.5 * nx)[:, None]
+    v = (np.arange(ny, dtype=np.float64) - 0.5 * ny)[None, :]
+    M = np.zeros((nx, ny, frames), np.complex64, order="F")
+    for f in range(frames):
+        th = 6.283185307179586476925286766559 * f / frames
+        m = np.zeros((nx, ny))
+        for amp, rad, ang, sig in blobs:
+            cu, cv = rad * np.cos(ang + th), rad * np.sin(ang + th)
+            m += amp * np.exp(-((u - cu) ** 2 + (v - cv) ** 2) / (2.0 * sig * sig))
+        M[:, :, f] = m.astype(np.float32)
+    L = float(min(nx, ny))
+    R, W = 0.5 * L, 0.4 * L
+    G = np.empty((nx, ny, coils))
+    be = 6.283185307179586476925286766559 * np.arange(coils) / coils
+    for c in range(coils):
+        G[:, :, c] = np.exp(-((u - R * np.cos(be[c])) ** 2 + (v - R * np.sin(be[c])) ** 2) / (2.0 * W * W))
+    G /= np.sqrt((G * G).sum(axis=2, keepdims=True))
+    S = np.asfortranarray((G * np.exp(1j * be)[None, None, :]).astype(np.complex64))
+    return sense_forward(M, S), S, M
+
+
 # ---------------------------------------------------------------------------
 # reference (the real library, oracle/_ref)
 # ---------------------------------------------------------------------------

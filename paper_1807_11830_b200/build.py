@@ -18,6 +18,7 @@ CSRC = os.path.join(PKG, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
 OBJ = os.path.join(ROOT, "build", "obj")
 LIB = os.path.join(PKG, "libhetreco_b200.so")
+CLI = os.path.join(PKG, "bin", "hetreco")
 CUDA = os.environ.get("CUDA_HOME", "/usr/local/cuda")
 NVCC = os.path.join(CUDA, "bin", "nvcc")
 
@@ -76,7 +77,26 @@ def build(force: bool = False, verbose: bool = True) -> str:
         os.replace(tmp, LIB)
         if verbose:
             print("built", LIB)
+    build_cli(force, verbose)
     return LIB
+
+
+def build_cli(force: bool = False, verbose: bool = True) -> str:
+    """The `hetreco` command-line front-end (csrc/cli), linked against the
+    exported C-ABI of libhetreco_b200.so (rpath $ORIGIN/..)."""
+    srcs = sorted(glob.glob(os.path.join(CSRC, "cli", "*.cpp")))
+    os.makedirs(os.path.dirname(CLI), exist_ok=True)
+    newest = max([os.path.getmtime(x) for x in srcs] + [os.path.getmtime(LIB), _headers_mtime()])
+    if not force and os.path.exists(CLI) and os.path.getmtime(CLI) >= newest:
+        return CLI
+    cmd = ["g++", "-std=c++20", "-O2", "-Wall", "-I", INCLUDE, "-o", CLI] + srcs + \
+        ["-L", PKG, "-l:libhetreco_b200.so", "-Wl,-rpath,$ORIGIN/.."]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"cli build failed: {' '.join(cmd)}\n{r.stdout}\n{r.stderr}")
+    if verbose:
+        print("built", CLI)
+    return CLI
 
 
 if __name__ == "__main__":

@@ -11,6 +11,7 @@
 
 #include "../kernels/launch.hpp"
 #include "hetreco_b200/io.hpp"
+#include "hetreco_b200/phantom.hpp"
 #include "hetreco_b200/processes.hpp"
 
 using namespace hetreco;
@@ -754,3 +755,28 @@ int hetreco_raw_write(const char* path, const char* sidecar_path, const hetreco_
 }
 
 }  // extern "C"
+
+// ---- gen_phantom (include/hetreco_b200/phantom.hpp) ------------------
+
+extern "C" int hetreco_gen_phantom(hetreco_session s, uint64_t nx, uint64_t ny, uint64_t frames, uint64_t coils,
+                                   uint64_t seed, void* kdata, void* smaps, void* truth) {
+    return guard([&] {
+        need(s, "session");
+        Phantom ph = gen_phantom(*s->s, PhantomSpec{nx, ny, frames, coils, seed});
+        auto put = [](void* dst, const Data& d) {
+            if (dst) std::memcpy(dst, d.arrays[0].bytes().data(), d.arrays[0].byte_size());
+        };
+        put(kdata, ph.kdata);
+        put(smaps, ph.smaps);
+        put(truth, ph.truth);
+    });
+}
+
+extern "C" int hetreco_phantom_blobs(uint64_t nx, uint64_t ny, uint64_t seed, double* out12) {
+    return guard([&] {
+        need(out12, "out");
+        const auto b = phantom_blobs(PhantomSpec{nx, ny, 1, 1, seed});
+        for (int i = 0; i < 3; ++i)
+            for (int j = 0; j < 4; ++j) out12[4 * i + j] = b[i][j];
+    });
+}

@@ -648,6 +648,19 @@ public:
                 throw ShapeMismatch(name() + ": s " + dims_str(sm) + " does not tile x " + dims_str(x));
             param_word = p.get_bool("conjugate_s", true) ? 1u : 0u;
             gsize_ = x.element_count();
+        } else if (which_ == dev::Builtin::MatrixAdd) {
+            // matrix_add(a, b) -> a + b (matrix_add.cl.src:5-24)
+            p.require_known({});
+            const LayoutRecord& b = array_of(li, 1, name());
+            if (x.element_type != ElementType::Float32 && x.element_type != ElementType::Float64 &&
+                x.element_type != ElementType::Int32)
+                throw UnsupportedElementType(name() + ": matrix_add takes FLOAT32, FLOAT64 or INT32 arrays");
+            require_type(b, x.element_type, name());
+            require_type(o, x.element_type, name());
+            if (b.dims != x.dims || o.dims != x.dims)
+                throw ShapeMismatch(name() + ": a " + dims_str(x) + ", b " + dims_str(b) + " and output " +
+                                    dims_str(o) + " must have equal shapes");
+            gsize_ = x.element_count();
         } else {
             p.require_known({});
             require_type(x, ElementType::Complex64, name());
@@ -845,9 +858,14 @@ public:
         nx_ = m.dims[0];
         ny_ = m.rank > 1 ? m.dims[1] : 1;
         nf_ = prod(m, 2, m.rank);
-        if (nx_ != ny_ || !is_pow2(nx_) || !dev::fft_size_supported(nx_))
-            throw ShapeMismatch(name() + ": images must be square with a power-of-two side <= 4096, got " +
-                                dims_str(m));
+        if (!is_pow2(nx_) || !is_pow2(ny_) || !dev::fft_size_supported(nx_) || !dev::fft_size_supported(ny_))
+            throw ShapeMismatch(name() + ": image sides must be powers of two <= 4096, got " + dims_str(m));
+        // the masked / round-trip column kernels are square-only; the plain
+        // forward model of a rectangular image uses the generic column pass
+        const bool masked = li.records.size() > 2;
+        generic_cols_ = nx_ != ny_;
+        if (generic_cols_ && (normal_ || masked))
+            throw ShapeMismatch(name() + ": masked and normal-operator models need square images, got " + dims_str(m));
         if (sm.dims[0] != nx_ || sm.dims[1] != ny_)
             throw ShapeMismatch(name() + ": sensitivity maps " + dims_str(sm) + " do not match image " + dims_str(m));
         nc_ = prod(sm, 2, sm.rank);
@@ -871,7 +889,12 @@ public:
         const int ord = session().cuda().ordinal(), sms = sm_count(ord);
         tw_fwd_ = twiddle_table(nx_, -1);
         s_exp_ = dev::plan_expand(nx_, ny_ * nc_ * nf_, sms);
-        s_col_ = dev::plan_strided_masked(ny_, normal_, nc_ * nf_, sms);
+        if (generic_cols_) {
+            tw_fwd_y_ = twiddle_table(ny_, -1);
+            s_col_ = dev::plan_strided(ny_, nx_, nc_ * nf_, sms);
+        } else {
+            s_col_ = dev::plan_strided_masked(ny_, normal_, nc_ * nf_, sms);
+        }
         if (normal_) {
             tw_inv_ = twiddle_table(nx_, +1);
             if (scratch_.size() != nx_ * ny_ * nc_ * nf_ * 8) scratch_ = DevMem(nx_ * ny_ * nc_ * nf_ * 8);
@@ -883,6 +906,12 @@ public:
         dev::ContigArgs ae{m_, z, s_, ny_, nc_, nf_, shift_, shift_, 1.0f, tw_fwd_.as<float2>()};
         ck(dev::launch_expand(nx_, ae, s_exp_, s), name() + "/expand+x-fft");
         mark(s);
+        if (generic_cols_) {
+            dev::StridedArgs ag{z, z, nx_, nc_ * nf_, shift_, shift_, 1.0f, tw_fwd_y_.as<float2>()};
+            ck(dev::launch_strided(ny_, -1, ag, s_col_, s), name() + "/y-fft");
+            mark(s);
+            return;
+        }
         dev::StridedArgs ac{z, z, nx_, nc_ * nf_, shift_, shift_, 1.0f, tw_fwd_.as<float2>(), mask_};
         ck(dev::launch_strided_masked(ny_, normal_, ac, s_col_, s), name() + (normal_ ? "/y-fft.mask.y-ifft" : "/y-fft.mask"));
         mark(s);
@@ -902,8 +931,9 @@ private:
     const float2* s_ = nullptr;
     const float* mask_ = nullptr;
     float2* out_ = nullptr;
-    DevMem tw_fwd_, tw_inv_, scratch_;
+    DevMem tw_fwd_, tw_fwd_y_, tw_inv_, scratch_;
     dev::LaunchShape s_exp_, s_col_, s_comb_;
+    bool generic_cols_ = false;
 };
 
 }  // namespace
@@ -916,6 +946,9 @@ std::unique_ptr<GraphProcess> make_fft2d(ComputeSession& s, std::string n) {
 }
 std::unique_ptr<GraphProcess> make_complex_element_prod(ComputeSession& s, std::string n) {
     return std::make_unique<BuiltinProcess>(s, std::move(n), dev::Builtin::ComplexElementProd);
+}
+std::unique_ptr<GraphProcess> make_matrix_add(ComputeSession& s, std::string n) {
+    return std::make_unique<BuiltinProcess>(s, std::move(n), dev::Builtin::MatrixAdd);
 }
 std::unique_ptr<GraphProcess> make_ximage_sum(ComputeSession& s, std::string n) {
     return std::make_unique<BuiltinProcess>(s, std::move(n), dev::Builtin::XImageSum);
@@ -936,6 +969,7 @@ std::unique_ptr<GraphProcess> make_process(ComputeSession& s, std::string_view k
     if (kind == "fft2d") return make_fft2d(s, n);
     if (kind == "complex_element_prod") return make_complex_element_prod(s, n);
     if (kind == "ximage_sum") return make_ximage_sum(s, n);
+    if (kind == "matrix_add") return make_matrix_add(s, n);
     if (kind == "rss_combine") return make_rss_combine(s, n);
     if (kind == "sens_recon") return make_sens_recon(s, n);
     if (kind == "rss_recon") return make_rss_recon(s, n);

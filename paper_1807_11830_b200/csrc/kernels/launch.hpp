@@ -154,4 +154,18 @@ LaunchShape plan_strided_masked(std::uint64_t N, bool roundtrip, std::uint64_t p
 cudaError_t launch_strided_masked(std::uint64_t N, bool roundtrip, const StridedArgs& a, const LaunchShape& s,
                                   cudaStream_t stream);
 
+// ---- synthetic phantom (phantom.cu) ------------------------------
+
+struct PhantomBlob {
+    double amp, radius, angle, sigma;  // pixels / radians, relative to the image centre
+};
+struct PhantomArgs {
+    float2* truth;  // [nx, ny, frames]
+    float2* smaps;  // [nx, ny, coils]
+    std::uint32_t nx, ny, frames, coils;
+    PhantomBlob blob[3];
+    double coil_radius, coil_width;
+};
+cudaError_t launch_phantom(const PhantomArgs& a, int device_sms, cudaStream_t st);
+
 }  // namespace hetreco::dev

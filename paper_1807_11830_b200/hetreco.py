@@ -87,6 +87,7 @@ EXPORTED = [
     "hetreco_session_timer_start", "hetreco_session_timer_stop",
     "hetreco_mat_read", "hetreco_mat_parse", "hetreco_image_read", "hetreco_raw_read", "hetreco_mat_count",
     "hetreco_mat_variable", "hetreco_mat_free", "hetreco_mat_write", "hetreco_image_write", "hetreco_raw_write",
+    "hetreco_gen_phantom", "hetreco_phantom_blobs",
 ]
 
 
@@ -146,6 +147,8 @@ def lib():
         "hetreco_mat_count": ([vp, vp], i32), "hetreco_mat_variable": ([vp, i32, vp, u64, vp], i32),
         "hetreco_mat_free": ([vp], i32), "hetreco_mat_write": ([pc, i32, vp, vp], i32),
         "hetreco_image_write": ([pc, vp], i32), "hetreco_raw_write": ([pc, pc, vp], i32),
+        "hetreco_gen_phantom": ([vp, u64, u64, u64, u64, u64, vp, vp, vp], i32),
+        "hetreco_phantom_blobs": ([u64, u64, u64, vp], i32),
     })
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -838,3 +841,21 @@ def write_raw(path: str, sidecar_path: str, array: np.ndarray) -> None:
     a = np.asfortranarray(array)
     _ck(lib().hetreco_raw_write(os.fsencode(path), os.fsencode(sidecar_path),
                                 C.byref(_desc(a.shape, a.dtype, a.ctypes.data))))
+
+
+def gen_phantom(session: "ComputeSession", nx: int = 128, ny: int = 128, frames: int = 16, coils: int = 8,
+                seed: int = 1):
+    """gen_phantom on the session's device -> (kdata Y, smaps S, truth M)."""
+    Y = np.empty((nx, ny, coils, frames), np.complex64, order="F")
+    S = np.empty((nx, ny, coils), np.complex64, order="F")
+    M = np.empty((nx, ny, frames), np.complex64, order="F")
+    _ck(lib().hetreco_gen_phantom(session._h, nx, ny, frames, coils, seed, Y.ctypes.data, S.ctypes.data,
+                                  M.ctypes.data))
+    return Y, S, M
+
+
+def phantom_blobs(nx: int, ny: int, seed: int):
+    """The seeded blob parameters gen_phantom uses: [(amp, radius, angle, sigma)] x 3."""
+    out = (C.c_double * 12)()
+    _ck(lib().hetreco_phantom_blobs(nx, ny, seed, out))
+    return [tuple(out[4 * i: 4 * i + 4]) for i in range(3)]

@@ -108,3 +108,18 @@ def test_c4_hundred_launches_after_one_init(s):
     assert st.init_calls == 1 and st.launches == 100
     assert s.counters() == {"host_to_device": 0, "device_to_host": 0}
     assert relmax(s.fetch_data(hout).arrays[0], o.sense_normal(M, S, mask)) <= TOL
+
+
+@pytest.mark.parametrize("nx,ny", [(64, 32), (32, 128), (256, 16)])
+def test_sense_forward_rectangular(s, nx, ny):
+    """Unmasked forward model on rectangular images (generic column pass);
+    masked / normal-operator models stay square-only."""
+    rng = np.random.default_rng(nx * 3 + ny)
+    M = cplx(rng, nx, ny, 2)
+    S = cplx(rng, nx, ny, 3)
+    Y, *_ = run(s, "sense_forward", [M, S], (nx, ny, 3, 2))
+    assert relmax(Y, o.sense_forward(M, S)) <= TOL
+    with pytest.raises(h.ShapeMismatch):
+        run(s, "sense_forward", [M, S, np.ones((nx, ny), np.float32)], (nx, ny, 3, 2))
+    with pytest.raises(h.ShapeMismatch):
+        run(s, "sense_normal", [M, S], (nx, ny, 2))
