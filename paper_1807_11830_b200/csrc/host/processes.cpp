@@ -511,9 +511,14 @@ public:
         nx_ = ri.dims[0];
         ny_ = ri.rank > 1 ? ri.dims[1] : 1;
         batch_ = prod(ri, 2, ri.rank);
-        if (!is_pow2(nx_) || !is_pow2(ny_))
-            throw ShapeMismatch(name() + ": spatial dims must be powers of two, got " + dims_str(ri));
-        radix2_ = algo == "radix2" || !dev::fft_size_supported(nx_) || !dev::fft_size_supported(ny_);
+        const bool p2 = is_pow2(nx_) && is_pow2(ny_);
+        const bool stockham_ok = dev::fft_size_supported(nx_) && dev::fft_size_supported(ny_);
+        if (!p2 && !stockham_ok)
+            throw ShapeMismatch(name() + ": spatial dims must be powers of two or mixed-radix sides (96, 160, 192, "
+                                         "320, 384), got " + dims_str(ri));
+        radix2_ = algo == "radix2" || !stockham_ok;
+        if (radix2_ && !p2)
+            throw ShapeMismatch(name() + ": the radix2 algorithm needs power-of-two dims, got " + dims_str(ri));
         if (radix2_ && shift_) throw InvalidParams(name() + ": shift requires the stockham algorithm");
         in_ = static_cast<const float2*>(session().device_array(require_input(), 0));
         out_ = static_cast<float2*>(session().device_array(require_output(), 0));
@@ -724,8 +729,8 @@ public:
         ny_ = y.dims[1];
         nc_ = y.dims[2];
         nf_ = prod(y, 3, y.rank);
-        if (!is_pow2(nx_) || !is_pow2(ny_) || !dev::fft_size_supported(nx_) || !dev::fft_size_supported(ny_))
-            throw ShapeMismatch(name() + ": spatial dims must be powers of two <= 4096, got " + dims_str(y));
+        if (!dev::fft_size_supported(nx_) || !dev::fft_size_supported(ny_))
+            throw ShapeMismatch(name() + ": spatial dims must be powers of two <= 4096 or mixed-radix sides (96, 160, 192, 320, 384), got " + dims_str(y));
         const LayoutRecord& o = array_of(output_layout(), 0, name());
         require_type(o, mode_ == dev::Combine::Sense ? ElementType::Complex64 : ElementType::Float32, name());
         if (o.dims[0] != nx_ || (o.rank > 1 ? o.dims[1] : 1) != ny_ || o.element_count() != nx_ * ny_ * nf_)
@@ -858,8 +863,8 @@ public:
         nx_ = m.dims[0];
         ny_ = m.rank > 1 ? m.dims[1] : 1;
         nf_ = prod(m, 2, m.rank);
-        if (!is_pow2(nx_) || !is_pow2(ny_) || !dev::fft_size_supported(nx_) || !dev::fft_size_supported(ny_))
-            throw ShapeMismatch(name() + ": image sides must be powers of two <= 4096, got " + dims_str(m));
+        if (!dev::fft_size_supported(nx_) || !dev::fft_size_supported(ny_))
+            throw ShapeMismatch(name() + ": image sides must be powers of two <= 4096 or mixed-radix sides (96, 160, 192, 320, 384), got " + dims_str(m));
         // the masked / round-trip column kernels are square-only; the plain
         // forward model of a rectangular image uses the generic column pass
         const bool masked = li.records.size() > 2;
@@ -998,8 +1003,8 @@ struct StreamingRecon::Impl {
 StreamingRecon::StreamingRecon(ComputeSession& s, Method method, std::uint64_t nx, std::uint64_t ny,
                                std::uint64_t coils, std::uint64_t chunk, const void* host_smaps, bool shift)
     : impl_(std::make_unique<Impl>()) {
-    if (!is_pow2(nx) || !is_pow2(ny) || !dev::fft_size_supported(nx) || !dev::fft_size_supported(ny))
-        throw ShapeMismatch("streaming recon: nx, ny must be powers of two <= 4096");
+    if (!dev::fft_size_supported(nx) || !dev::fft_size_supported(ny))
+        throw ShapeMismatch("streaming recon: nx, ny must be powers of two <= 4096 or mixed-radix sides (96, 160, 192, 320, 384)");
     if (coils == 0 || chunk == 0) throw InvalidArgument("streaming recon: coils and chunk_frames must be >= 1");
     Impl& m = *impl_;
     m.session = &s;

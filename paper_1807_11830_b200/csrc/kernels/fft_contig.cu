@@ -69,7 +69,7 @@ cudaError_t launch_contig(std::uint64_t N, int dir, Combine mode, const ContigAr
     const int T = int(N) / s.rq;
     const int lpb = s.block / T;
     const std::uint64_t items64 = a.ny * a.frames;
-    if (items64 >= (std::uint64_t(1) << 32) || (a.ny & (a.ny - 1))) return cudaErrorInvalidValue;
+    if (items64 >= (std::uint64_t(1) << 32)) return cudaErrorInvalidValue;
     const std::uint32_t items = std::uint32_t(items64);
     if (mode != Combine::None) {
         if (dir < 0) return cudaErrorInvalidValue;

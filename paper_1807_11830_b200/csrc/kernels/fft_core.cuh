@@ -101,12 +101,43 @@ __device__ __forceinline__ float2 wmul(float2 v) {
     }
 }
 
+// i * DIR * v  (multiplication by +-i)
+template <int DIR>
+__device__ __forceinline__ float2 mul_i(float2 v) {
+    return DIR > 0 ? make_float2(-v.y, v.x) : make_float2(v.y, -v.x);
+}
+
 // In-register DFT of Rp points stored at v[OFF + q*STR], q = 0..Rp-1, natural
-// order in and out.  Radix-2 decimation in time.
+// order in and out.  Radix-2 decimation in time for powers of two; direct
+// symmetric butterflies for 3 and 5 (W = e^{DIR 2 pi i / Rp}).
 template <int Rp, int DIR, int STR, int OFF, int R>
 __device__ __forceinline__ void dft_regs(float2 (&v)[R]) {
     if constexpr (Rp == 1) {
         return;
+    } else if constexpr (Rp == 3) {
+        constexpr float c = -0.5f, sn = 0.86602540378443864676f;  // cos, sin(2 pi / 3)
+        const float2 a0 = v[OFF], a1 = v[OFF + STR], a2 = v[OFF + 2 * STR];
+        const float2 t1 = cadd(a1, a2), t2 = csub(a1, a2);
+        const float2 m = make_float2(fmaf(c, t1.x, a0.x), fmaf(c, t1.y, a0.y));
+        const float2 r = mul_i<DIR>(cscale(t2, sn));
+        v[OFF] = cadd(a0, t1);
+        v[OFF + STR] = cadd(m, r);
+        v[OFF + 2 * STR] = csub(m, r);
+    } else if constexpr (Rp == 5) {
+        constexpr float c1 = 0.30901699437494742410f, c2 = -0.80901699437494742410f;  // cos(2pi/5), cos(4pi/5)
+        constexpr float s1 = 0.95105651629515357212f, s2 = 0.58778525229247312917f;   // sin(2pi/5), sin(4pi/5)
+        const float2 a0 = v[OFF], a1 = v[OFF + STR], a2 = v[OFF + 2 * STR], a3 = v[OFF + 3 * STR],
+                     a4 = v[OFF + 4 * STR];
+        const float2 t1 = cadd(a1, a4), t2 = cadd(a2, a3), t3 = csub(a1, a4), t4 = csub(a2, a3);
+        const float2 m1 = make_float2(fmaf(c1, t1.x, fmaf(c2, t2.x, a0.x)), fmaf(c1, t1.y, fmaf(c2, t2.y, a0.y)));
+        const float2 m2 = make_float2(fmaf(c2, t1.x, fmaf(c1, t2.x, a0.x)), fmaf(c2, t1.y, fmaf(c1, t2.y, a0.y)));
+        const float2 r1 = mul_i<DIR>(make_float2(fmaf(s1, t3.x, s2 * t4.x), fmaf(s1, t3.y, s2 * t4.y)));
+        const float2 r2 = mul_i<DIR>(make_float2(fmaf(s2, t3.x, -s1 * t4.x), fmaf(s2, t3.y, -s1 * t4.y)));
+        v[OFF] = cadd(a0, cadd(t1, t2));
+        v[OFF + STR] = cadd(m1, r1);
+        v[OFF + 4 * STR] = csub(m1, r1);
+        v[OFF + 2 * STR] = cadd(m2, r2);
+        v[OFF + 3 * STR] = csub(m2, r2);
     } else {
         constexpr int bits = ilog2c(Rp);
         float2 a[Rp];
@@ -148,28 +179,50 @@ __device__ __forceinline__ void slots(bool rot, F&& fn) {
 // default R is 16 for N >= 128 (two passes at 256, one shared-memory
 // exchange) and 8 below; kernels may ask for R = 8 at N >= 128 (more passes,
 // fewer registers per thread).
+//
+// Mixed radix (N = 3 * 2^k or 5 * 2^k, e.g. the paper's 160 x 160 cine; the
+// reference is radix-2 only): one radix-3/5 pass, then
+// radix-4 passes and a remainder, with R = 3*4 or 5*4 points per thread so
+// every pass radix divides R.  The pass twiddles of these sizes are read from
+// the (L1-resident) W_N^t table at the point of use instead of being held in
+// registers.
 constexpr int default_points(int N) { return N <= 16 ? N : (N <= 64 ? 8 : 16); }
+
+constexpr int odd_part(int N) { return (N > 0 && N % 2 == 0) ? odd_part(N / 2) : N; }
+constexpr bool is_mixed_size(int N) { return odd_part(N) != 1; }
 
 template <int N, int RQ>
 struct Plan {
-    static constexpr int R = RQ < N ? RQ : N;
+    static constexpr int M = odd_part(N);  // 1 (power of two), 3 or 5
+    static_assert(M == 1 || M == 3 || M == 5, "FFT sizes are 2^k, 3*2^k or 5*2^k");
+    static constexpr int Q = M == 1 ? 0 : (N / M >= 4 ? 4 : N / M);
+    static constexpr int R = M == 1 ? (RQ < N ? RQ : N) : M * Q;
+    static constexpr int first = M == 1 ? R : M;  // radix of pass 0
+    static constexpr int step = M == 1 ? R : Q;   // radix of the passes after it
+    static constexpr int radix(int p) {
+        int n = N;
+        for (int i = 0; i <= p; ++i) {
+            const int r = i == 0 ? (first < n ? first : n) : (n >= step ? step : n);
+            if (i == p) return r;
+            n /= r;
+        }
+        return 1;
+    }
     static constexpr int count_passes() {
         int n = N, p = 0;
         while (n > 1) {
-            n = n >= R ? n / R : 1;
+            n /= radix(p);
             ++p;
         }
         return p;
     }
     static constexpr int P = count_passes();
-    static constexpr int radix(int p) {
-        int n = N;
-        for (int i = 0; i < p; ++i) n = n >= R ? n / R : 1;
-        return n >= R ? R : n;
-    }
 };
 
-template <int N, int RQ = default_points(N)>
+// TWREG: pass twiddles held in registers (default for powers of two) or read
+// from the W_N^t table at the point of use (default for mixed radix, whose
+// plans need up to 40 twiddles per thread).
+template <int N, int RQ = default_points(N), bool TWREG = !is_mixed_size(N)>
 struct LineFFT {
     using PL = Plan<N, RQ>;
     static constexpr int R = PL::R;
@@ -182,6 +235,18 @@ struct LineFFT {
     static constexpr int tw_count(int p) { return p == 0 ? 0 : (R / radix(p)) * (radix(p) - 1); }
     static constexpr int tw_offset(int p) { return p <= 1 ? 0 : tw_offset(p - 1) + tw_count(p - 1); }
     static constexpr int NTW = P == 0 ? 1 : tw_offset(P - 1) + tw_count(P - 1) + 1;
+    static constexpr bool kTableTw = !TWREG;  // table twiddles
+
+    // Pass twiddles of a thread: registers (powers of two) or a reference to
+    // the W_N^t table (mixed radix).
+    struct RegTwiddles {
+        float2 w[NTW];
+    };
+    struct TableTwiddles {
+        const float2* __restrict__ table;
+        float scale;
+    };
+    using Twiddles = std::conditional_t<kTableTw, TableTwiddles, RegTwiddles>;
 
     // Padded shared-memory index: one 8-byte pad per 16 samples.
     __device__ __forceinline__ static int pad(int p) { return p + (p >> 4); }
@@ -190,8 +255,18 @@ struct LineFFT {
     // Loads this thread's pass twiddles from the W_N^t table (DIR applied).
     // The last pass' twiddles are pre-multiplied by `scale` so run() applies
     // the normalisation for free (only the q = 0 slots need an explicit FMUL).
-    __device__ __forceinline__ static void load_twiddles(float2 (&tw)[NTW], const float2* __restrict__ table,
-                                                         int j, float scale = 1.0f) {
+    __device__ __forceinline__ static void load_twiddles(Twiddles& twd, const float2* __restrict__ table, int j,
+                                                         float scale = 1.0f) {
+        if constexpr (kTableTw) {
+            twd.table = table;
+            twd.scale = scale;
+            return;
+        } else {
+            load_twiddles_regs(twd.w, table, j, scale);
+        }
+    }
+    __device__ __forceinline__ static void load_twiddles_regs(float2 (&tw)[NTW], const float2* __restrict__ table,
+                                                              int j, float scale) {
         sfor<P>([&](auto pc) {
             constexpr int p = pc.value;
             if constexpr (p >= 1) {
@@ -216,14 +291,25 @@ struct LineFFT {
     // The output is multiplied by `scale`, which must be the value the
     // twiddles were loaded with.
     template <int DIR, class Sync>
-    __device__ __forceinline__ static void run(float2 (&v)[R], const float2 (&tw)[NTW], float2* line, int j,
+    __device__ __forceinline__ static void run(float2 (&v)[R], const Twiddles& twd, float2* line, int j,
                                                Sync&& sync, float scale = 1.0f) {
-        run_f<DIR>(
-            v,
-            [&](auto pc, auto sc, auto qc) {
-                return tw[tw_offset(pc.value) + sc.value * (radix(pc.value) - 1) + qc.value];
-            },
-            line, j, sync, scale);
+        if constexpr (kTableTw) {
+            run_f<DIR>(
+                v,
+                [&](auto pc, auto sc, auto qc) {
+                    float2 w = __ldg(twd.table + tw_index<pc.value, sc.value, qc.value>(j));
+                    if constexpr (pc.value == P - 1) w = make_float2(w.x * twd.scale, w.y * twd.scale);
+                    return w;
+                },
+                line, j, sync, scale);
+        } else {
+            run_f<DIR>(
+                v,
+                [&](auto pc, auto sc, auto qc) {
+                    return twd.w[tw_offset(pc.value) + sc.value * (radix(pc.value) - 1) + qc.value];
+                },
+                line, j, sync, scale);
+        }
     }
 
     // Twiddle for pass p (>= 1), sub-group s, q = qc + 1 of thread j from a

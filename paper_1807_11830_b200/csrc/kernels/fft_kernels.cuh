@@ -25,6 +25,28 @@
 
 namespace hetreco::dev {
 
+// item -> (item / d, item % d): shift/mask when d is a power of two (the
+// common case), a 32-bit division otherwise (mixed-radix image sides).
+struct IndexSplit {
+    std::uint32_t d;
+    int shift;  // -1: not a power of two
+    __host__ __device__ __forceinline__ explicit IndexSplit(std::uint32_t d_) : d(d_), shift(-1) {
+        if (d_ && !(d_ & (d_ - 1))) {
+            shift = 0;
+            while ((1u << shift) < d_) ++shift;
+        }
+    }
+    __device__ __forceinline__ void split(std::uint32_t item, std::uint32_t& q, std::uint32_t& r) const {
+        if (shift >= 0) {
+            q = item >> shift;
+            r = item & (d - 1);
+        } else {
+            q = item / d;
+            r = item - q * d;
+        }
+    }
+};
+
 template <int N>
 constexpr int line_stride() {
     return (LineFFT<N>::padded_len) | 1;  // odd: spreads lines over banks
@@ -46,17 +68,18 @@ __global__ void __launch_bounds__(MINB > 1 ? 256 : 512, MINB > 1 ? MINB : 0) k_f
     const int tid = threadIdx.x;
     const int l = tid % tx, j = tid / tx;
     float2* line = smem + l * line_stride<N>();
-    float2 tw[L::NTW];
+    typename L::Twiddles tw;
     L::load_twiddles(tw, a.tw, j, a.scale);
     const std::uint32_t nx = NXC ? std::uint32_t(NXC) : std::uint32_t(a.nx);
     const std::uint32_t xtiles = nx / std::uint32_t(tx);
-    const int lx = __ffs(xtiles) - 1;
+    const IndexSplit xsplit(xtiles);
     const std::uint64_t plane_elems = std::uint64_t(nx) * N;
     const std::uint32_t step = std::uint32_t(T) * nx;  // slot-to-slot distance (runtime variant)
     const bool sh_in = a.shift_in, sh_out = a.shift_out;
     auto tile_off = [&](std::uint32_t tile) {
-        const std::uint32_t plane = tile >> lx;
-        const std::uint32_t col = (tile & (xtiles - 1)) * std::uint32_t(tx) + std::uint32_t(l);
+        std::uint32_t plane, xt;
+        xsplit.split(tile, plane, xt);
+        const std::uint32_t col = xt * std::uint32_t(tx) + std::uint32_t(l);
         return std::uint64_t(plane) * plane_elems + col + std::uint32_t(j) * nx;
     };
     auto load = [&](std::uint64_t off, float2(&v)[R]) {
@@ -118,7 +141,7 @@ __global__ void __launch_bounds__(256) k_fft_contig(ContigArgs a, int lpb, std::
     const int tid = threadIdx.x;
     const int j = tid % T, l = tid / T;
     float2* line = smem + l * line_stride<N>();
-    float2 tw[L::NTW];
+    typename L::Twiddles tw;
     L::load_twiddles(tw, a.tw, j, a.scale);
     const bool sh_in = a.shift_in, sh_out = a.shift_out;
     for (std::uint32_t grp = blockIdx.x; grp * lpb < items; grp += gridDim.x) {
@@ -154,19 +177,19 @@ __global__ void __launch_bounds__(MINB > 1 ? 128 : 256, MINB > 1 ? MINB : 0) k_f
     const int tid = threadIdx.x;
     const int j = tid % T, l = tid / T;
     float2* line = smem + l * line_stride<N>();
-    float2 tw[L::NTW];
+    typename L::Twiddles tw;
     L::load_twiddles(tw, a.tw, j, a.scale);
     const bool sh_in = a.shift_in, sh_out = a.shift_out;
     const std::uint32_t C = std::uint32_t(a.coils);
     const std::uint32_t ny = std::uint32_t(a.ny);
-    const int ly = __ffs(ny) - 1;                           // ny is a power of two
+    const IndexSplit ysplit(ny);
     const std::uint64_t coil_stride = std::uint64_t(ny) * N;  // elements between coils (X and S)
     for (std::uint32_t grp = blockIdx.x; grp * lpb < items; grp += gridDim.x) {
         const std::uint32_t item = grp * lpb + l;
         const bool active = item < items;
         // inactive lines re-read line 0 (valid memory) and skip the store
-        const std::uint32_t y = active ? (item & (ny - 1)) : 0;
-        const std::uint32_t f = active ? (item >> ly) : 0;
+        std::uint32_t f, y;
+        ysplit.split(active ? item : 0u, f, y);
         const float2* xbase = a.in + (std::uint64_t(f) * C * ny + y) * N + j;
         const float2* sbase = a.smap + std::uint64_t(y) * N + j;
         auto load_x = [&](std::uint32_t c, float2(&d)[R]) {
@@ -281,8 +304,11 @@ __global__ void __launch_bounds__(MINB > 1 ? 128 : 256, MINB > 1 ? MINB : 0) k_f
 
 // ---- shared dispatch helpers ----------------------------------------------------------------
 
+// Powers of two, plus the mixed-radix sides 3*2^k / 5*2^k of common MR
+// matrices (96, 160 -- the paper's cine --, 192, 320, 384).
 #define HETRECO_FFT_SIZES(X) \
-    X(1) X(2) X(4) X(8) X(16) X(32) X(64) X(128) X(256) X(512) X(1024) X(2048) X(4096)
+    X(1) X(2) X(4) X(8) X(16) X(32) X(64) X(128) X(256) X(512) X(1024) X(2048) X(4096) \
+    X(96) X(160) X(192) X(320) X(384)
 
 // Sizes that also get the tuning variants (R = 8 plans, register prefetch).
 template <int N>

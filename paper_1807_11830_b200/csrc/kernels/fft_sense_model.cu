@@ -31,16 +31,17 @@ __global__ void __launch_bounds__(256) k_fft_expand(ContigArgs a, int lpb, std::
     const int tid = threadIdx.x;
     const int j = tid % T, l = tid / T;
     float2* line = smem + l * line_stride<N>();
-    float2 tw[L::NTW];
+    typename L::Twiddles tw;
     L::load_twiddles(tw, a.tw, j, 1.0f);
     const bool sh_in = a.shift_in, sh_out = a.shift_out;
     const std::uint32_t ny = std::uint32_t(a.ny), C = std::uint32_t(a.coils);
-    const int ly = __ffs(ny) - 1;
+    const IndexSplit ysplit(ny);
     for (std::uint32_t grp = blockIdx.x; grp * lpb < items; grp += gridDim.x) {
         const std::uint32_t item = grp * lpb + l;  // = y + ny * (c + C * f)
         const bool active = item < items;
         const std::uint32_t it = active ? item : 0;
-        const std::uint32_t y = it & (ny - 1), rest = it >> ly;
+        std::uint32_t y, rest;
+        ysplit.split(it, rest, y);
         const std::uint32_t c = rest % C, f = rest / C;
         const float2* mrow = a.in + (std::uint64_t(f) * ny + y) * N + j;
         const float2* srow = a.smap + (std::uint64_t(c) * ny + y) * N + j;
@@ -61,15 +62,16 @@ __global__ void __launch_bounds__(256) k_fft_strided_masked(StridedArgs a, int t
     const int tid = threadIdx.x;
     const int l = tid % tx, j = tid / tx;
     float2* line = smem + l * line_stride<N>();
-    float2 tw[L::NTW];  // forward twiddles, scale 1
+    typename L::Twiddles tw;  // forward twiddles, scale 1
     L::load_twiddles(tw, a.tw, j, 1.0f);
     const std::uint32_t xtiles = NX / std::uint32_t(tx);
-    const int lx = __ffs(xtiles) - 1;
+    const IndexSplit xsplit(xtiles);
     const bool sh_in = a.shift_in, sh_out = a.shift_out;
     const float scale = a.scale;
     for (std::uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        const std::uint32_t plane = tile >> lx;
-        const std::uint32_t col = (tile & (xtiles - 1)) * std::uint32_t(tx) + std::uint32_t(l);
+        std::uint32_t plane, xt;
+        xsplit.split(tile, plane, xt);
+        const std::uint32_t col = xt * std::uint32_t(tx) + std::uint32_t(l);
         const std::uint64_t off = std::uint64_t(plane) * NX * N + col + std::uint32_t(j) * NX;
         const float2* src = a.in + off;
         float2 v[R];
@@ -156,7 +158,7 @@ cudaError_t launch_expand(std::uint64_t N, const ContigArgs& a, const LaunchShap
     const int T = int(N) / s.rq;
     const int lpb = s.block / T;
     const std::uint64_t items64 = a.ny * a.coils * a.frames;
-    if (items64 >= (std::uint64_t(1) << 32) || (a.ny & (a.ny - 1))) return cudaErrorInvalidValue;
+    if (items64 >= (std::uint64_t(1) << 32)) return cudaErrorInvalidValue;
     const std::uint32_t items = std::uint32_t(items64);
     switch (N) {
 #define X(n) \

@@ -241,11 +241,16 @@ def test_fft2d_shift_is_exact_permutation(s):
 
 
 def test_fft2d_rejects_bad_shapes_and_params(s):
-    x = np.zeros((160, 160), np.complex64)
+    x = np.zeros((100, 100), np.complex64)  # neither 2^k nor a mixed-radix side
+    hin = s.register_data([x])
+    hout = s.allocate_data([((100, 100), np.complex64)])
+    with pytest.raises(h.ShapeMismatch):
+        h.Process(s, "fft2d").set_input(hin).set_output(hout).init()
+    x = np.zeros((160, 160), np.complex64)  # mixed radix: stockham only
     hin = s.register_data([x])
     hout = s.allocate_data([((160, 160), np.complex64)])
     with pytest.raises(h.ShapeMismatch):
-        h.Process(s, "fft2d").set_input(hin).set_output(hout).init()
+        h.Process(s, "fft2d").set_input(hin).set_output(hout).init({"algorithm": "radix2"})
     y = s.register_data([np.zeros((16, 16), np.complex64)])
     z = s.allocate_data([((16, 8), np.complex64)])
     with pytest.raises(h.ShapeMismatch):
