@@ -144,7 +144,9 @@ int hetreco_copy_array(hetreco_session s, hetreco_handle src, uint64_t src_index
 /* load_builtin_kernels / kernels().names() (session.hpp:94-101); names '\n'-joined */
 int hetreco_load_builtin_kernels(hetreco_session s);
 int hetreco_kernel_names(hetreco_session s, char* buf, uint64_t cap);
-/* load_kernels(units) (session.hpp:97): always UnsupportedSource on this build */
+/* load_kernels(units) (session.hpp:97): kernel-source units (the reference's
+ * HETRECO_KERNEL dialect) compiled by NVRTC for sm_100a; CompileError carries
+ * every failing unit's log, DuplicateKernel leaves the registry unchanged. */
 int hetreco_load_kernels(hetreco_session s, int count, const char* const* unit_names, const char* const* sources);
 /* launch_kernel (session.hpp:108-109; session.cpp:154-169) */
 int hetreco_launch_kernel(hetreco_session s, const char* name, hetreco_handle in, hetreco_handle out,
@@ -251,6 +253,14 @@ int hetreco_gen_phantom(hetreco_session s, uint64_t nx, uint64_t ny, uint64_t fr
                         uint64_t seed, void* kdata, void* smaps, void* truth);
 /* the seeded blob parameters (amp, radius, angle, sigma) x 3 -- host only */
 int hetreco_phantom_blobs(uint64_t nx, uint64_t ny, uint64_t seed, double* out12);
+
+/* ---- source kernels (cpujit_backend.cpp:121-177 role) --------
+ * Compile one unit with NVRTC for sm_100a without loading it (no device
+ * needed): names = its kernels, '\n'-joined; log = compiler output (the
+ * failure log on CompileError). */
+int hetreco_nvrtc_compile_check(const char* unit_name, const char* source, char* names, uint64_t names_cap,
+                                char* log, uint64_t log_cap);
+int hetreco_nvrtc_available(int* available);
 
 #if defined(__GNUC__)
 #pragma GCC visibility pop

@@ -28,6 +28,8 @@
 
 typedef struct CUstream_st* cudaStream_t;
 typedef struct CUevent_st* cudaEvent_t;
+typedef struct CUkern_st* cudaKernel_t;
+typedef struct CUlib_st* cudaLibrary_t;
 
 namespace hetreco {
 
@@ -170,7 +172,9 @@ public:
     std::string_view id() const override { return id_; }
     std::vector<DeviceDescriptor> devices() const override { return {desc_}; }
     TransferPath transfer_path() const override { return TransferPath::Staged; }
-    bool supports_source_kernels() const override { return false; }
+    // true when NVRTC is available: compile() builds kernel-source units for
+    // sm_100a at run time (the reference's cpujit role)
+    bool supports_source_kernels() const override;
 
     BufferId allocate(std::uint64_t bytes) override;
     void release(BufferId buffer) override;
@@ -219,6 +223,10 @@ private:
     std::byte* ring_dev_ = nullptr;
     std::uint64_t ring_size_ = 0, ring_head_ = 0;
     mutable std::string last_kernel_;
+    // run-time compiled (NVRTC) kernels: "<unit tag>/<name>" -> entry point
+    std::unordered_map<std::string, cudaKernel_t> jit_;
+    std::vector<cudaLibrary_t> jit_libs_;
+    std::uint64_t jit_units_ = 0;
 };
 
 // Number of CUDA devices visible to this process (0 when no driver/GPU).

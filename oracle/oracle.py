@@ -103,6 +103,11 @@ def reference():
             lib.refdrv_recon_e2e.argtypes = [_i32, _vp, _vp, _vp, _u64, _u64, _u64, _u64, _i32,
                                              C.POINTER(_f64)]
             lib.refdrv_layout_header.argtypes = [_i32, _vp, _vp, _vp, _u64, _vp, C.POINTER(_u64)]
+            if hasattr(lib, "refdrv_builtin_source_count"):
+                lib.refdrv_builtin_source_name.restype = C.c_char_p
+                lib.refdrv_builtin_source_name.argtypes = [_i32]
+                lib.refdrv_builtin_source_text.restype = C.c_char_p
+                lib.refdrv_builtin_source_text.argtypes = [_i32]
             _ref = lib
         return _ref
 
@@ -417,6 +422,14 @@ def ref_recon_e2e(method: str, Y: np.ndarray, S: np.ndarray | None = None, reps:
                                             _p(S) if S is not None else None, _p(out), nx, ny, nc, nf,
                                             reps, C.byref(mean_s)))
     return out, mean_s.value
+
+
+def ref_builtin_sources():
+    """The reference library's embedded builtin kernel units [(unit_name, text)]
+    (kernels.hpp:52-57) -- inputs for source-kernel equivalence tests."""
+    L = reference()
+    return [(L.refdrv_builtin_source_name(i).decode(), L.refdrv_builtin_source_text(i).decode())
+            for i in range(L.refdrv_builtin_source_count())]
 
 
 def ref_pool_threads() -> int:

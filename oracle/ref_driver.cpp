@@ -333,4 +333,11 @@ int REFDRV(layout_header)(int count, const int* types, const int* ranks, const u
     });
 }
 
+// The reference's embedded builtin kernel sources (kernels.hpp:52-57,
+// builtin_kernel_sources()) -- fed to the B200 NVRTC path by the tests to
+// pin source-kernel equivalence with the precompiled builtins.
+int REFDRV(builtin_source_count)() { return int(builtin_kernel_sources().size()); }
+const char* REFDRV(builtin_source_name)(int i) { return builtin_kernel_sources()[std::size_t(i)].unit_name.c_str(); }
+const char* REFDRV(builtin_source_text)(int i) { return builtin_kernel_sources()[std::size_t(i)].source_text.c_str(); }
+
 }  // extern "C"

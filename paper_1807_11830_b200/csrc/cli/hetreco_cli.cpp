@@ -10,6 +10,7 @@
 //                       [--shift] [--device F]
 //   hetreco bench --op fft|rss|sens|negate|matadd --sizes L --repeats N [--device F]
 //                 [--csv path] [--deterministic-timing]
+//   hetreco compile --source unit.cl.src [--source ...]
 //
 // Built against the exported C-ABI only (include/hetreco_b200.h), like any
 // reference-side binding.  Every command exits 0 on success, nonzero with a
@@ -443,6 +444,46 @@ int cmd_bench(const Args& a) {
     return 0;
 }
 
+// Compiles kernel-source units for sm_100a (NVRTC; no device needed) and lists
+// their kernels.  A failing unit's compiler log is printed verbatim and the
+// command exits nonzero ("error log is immediately available").
+int cmd_compile(int argc, char** argv) {
+    std::vector<std::string> files;
+    for (int i = 2; i < argc; ++i) {
+        const std::string a = argv[i];
+        if (a == "--source" && i + 1 < argc) {
+            files.push_back(argv[++i]);
+        } else {
+            throw Fail("usage: hetreco compile --source unit.cl.src [--source ...]", 2);
+        }
+    }
+    if (files.empty()) throw Fail("missing required option --source", 2);
+    int failed = 0;
+    for (const std::string& f : files) {
+        FILE* fp = std::fopen(f.c_str(), "rb");
+        if (!fp) throw Fail("cannot read " + f, 3);
+        std::string src;
+        char buf[4096];
+        std::size_t n;
+        while ((n = std::fread(buf, 1, sizeof buf, fp)) > 0) src.append(buf, n);
+        std::fclose(fp);
+        std::vector<char> names(8192), log(1 << 20);
+        const std::string unit = f.substr(f.find_last_of('/') == std::string::npos ? 0 : f.find_last_of('/') + 1);
+        const int rc = hetreco_nvrtc_compile_check(unit.c_str(), src.c_str(), names.data(), names.size(), log.data(),
+                                                   log.size());
+        if (rc != HETRECO_OK) {
+            std::fprintf(stderr, "hetreco compile: %s: %s\n", unit.c_str(), hetreco_last_error());
+            ++failed;
+            continue;
+        }
+        std::string ns = names.data();
+        for (char& c : ns)
+            if (c == '\n') c = ' ';
+        std::printf("%s: %s\n", unit.c_str(), ns.c_str());
+    }
+    return failed ? 4 : 0;
+}
+
 void usage() {
     std::fprintf(stderr,
                  "usage: hetreco <command> [options]\n"
@@ -452,7 +493,8 @@ void usage() {
                  "--out-truth t.mat\n"
                  "  reconstruct --kdata k.mat [--smaps s.mat] --method sens|rss --output o.mat [--shift]\n"
                  "  bench --op fft|rss|sens|negate|matadd --sizes L --repeats N [--csv path] "
-                 "[--deterministic-timing]\n");
+                 "[--deterministic-timing]\n"
+                 "  compile --source unit.cl.src [--source ...]   (NVRTC, sm_100a)\n");
 }
 
 }  // namespace
@@ -469,6 +511,7 @@ int main(int argc, char** argv) {
         if (cmd == "gen-phantom") return cmd_gen_phantom(parse(argc, argv, {}));
         if (cmd == "reconstruct") return cmd_reconstruct(parse(argc, argv, {"shift"}));
         if (cmd == "bench") return cmd_bench(parse(argc, argv, {"deterministic-timing"}));
+        if (cmd == "compile") return cmd_compile(argc, argv);
         if (cmd == "--help" || cmd == "-h" || cmd == "help") {
             usage();
             return 0;

@@ -12,6 +12,7 @@
 #include "../kernels/launch.hpp"
 #include "hetreco_b200/io.hpp"
 #include "hetreco_b200/phantom.hpp"
+#include "nvrtc_compiler.hpp"
 #include "hetreco_b200/processes.hpp"
 
 using namespace hetreco;
@@ -778,5 +779,33 @@ extern "C" int hetreco_phantom_blobs(uint64_t nx, uint64_t ny, uint64_t seed, do
         const auto b = phantom_blobs(PhantomSpec{nx, ny, 1, 1, seed});
         for (int i = 0; i < 3; ++i)
             for (int j = 0; j < 4; ++j) out12[4 * i + j] = b[i][j];
+    });
+}
+
+// ---- source kernels: compile-only check (no device needed) ---------------------------
+
+extern "C" int hetreco_nvrtc_compile_check(const char* unit_name, const char* source, char* names, uint64_t names_cap,
+                                           char* log, uint64_t log_cap) {
+    return guard([&] {
+        need(unit_name, "unit_name");
+        need(source, "source");
+        nvrtc::Unit u;
+        try {
+            u = nvrtc::compile(unit_name, source, "sm_100a");
+        } catch (const CompileError& e) {
+            if (log && log_cap) copy_str(log, log_cap, e.diagnostics().empty() ? e.what() : e.diagnostics()[0].log);
+            throw;
+        }
+        std::string joined;
+        for (const auto& k : u.kernels) joined += (joined.empty() ? "" : "\n") + k;
+        if (names && names_cap) copy_str(names, names_cap, joined);
+        if (log && log_cap) copy_str(log, log_cap, u.log);
+    });
+}
+
+extern "C" int hetreco_nvrtc_available(int* available) {
+    return guard([&] {
+        need(available, "available");
+        *available = nvrtc::available() ? 1 : 0;
     });
 }

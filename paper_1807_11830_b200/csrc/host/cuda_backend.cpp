@@ -10,6 +10,8 @@
 #include "../kernels/launch.hpp"
 #include "hetreco_b200/runtime.hpp"
 
+#include "nvrtc_compiler.hpp"
+
 namespace hetreco {
 
 namespace {
@@ -61,7 +63,7 @@ CudaBackend::CudaBackend(int ordinal, std::uint64_t capacity) : ordinal_(ordinal
     desc_.api_version = std::to_string(p.major) + "." + std::to_string(p.minor);
     desc_.global_memory_bytes = capacity ? capacity : std::uint64_t(p.totalGlobalMem);
     desc_.base_alignment_bytes = 256;
-    desc_.supports_source_kernels = false;
+    desc_.supports_source_kernels = nvrtc::available();
     make_current();
     ck(cudaStreamCreateWithFlags(&compute_, cudaStreamNonBlocking), "cudaStreamCreate");
     ck(cudaStreamCreateWithFlags(&h2d_, cudaStreamNonBlocking), "cudaStreamCreate");
@@ -84,6 +86,7 @@ CudaBackend::~CudaBackend() {
     cudaStreamDestroy(compute_);
     cudaStreamDestroy(h2d_);
     cudaStreamDestroy(d2h_);
+    for (cudaLibrary_t l : jit_libs_) cudaLibraryUnload(l);
 }
 
 void CudaBackend::make_current() const { ck(cudaSetDevice(ordinal_), "cudaSetDevice"); }
@@ -176,9 +179,49 @@ std::vector<CompiledKernel> CudaBackend::intrinsic_kernels() {
     return ks;
 }
 
-std::vector<CompiledKernel> CudaBackend::compile(std::span<const ProgramSource>) {
-    throw UnsupportedSource("backend '" + id_ +
-                            "' runs precompiled sm_100a kernels and cannot compile kernel source");
+bool CudaBackend::supports_source_kernels() const { return nvrtc::available(); }
+
+// Kernel-source units -> NVRTC sm_100a cubins -> loaded libraries.  All units
+// compile before any loads (a failure anywhere throws CompileError carrying
+// every failing unit's log, and nothing is registered: the registry's
+// all-or-nothing rule, kernels.hpp:27-32).
+std::vector<CompiledKernel> CudaBackend::compile(std::span<const ProgramSource> units) {
+    if (!nvrtc::available())
+        throw UnsupportedSource("backend '" + id_ + "': NVRTC is not available, kernel source cannot be compiled");
+    std::vector<nvrtc::Unit> built;
+    std::vector<BuildDiagnostic> failures;
+    for (const ProgramSource& u : units) {
+        try {
+            built.push_back(nvrtc::compile(u.unit_name, u.source_text, "sm_100a"));
+        } catch (const CompileError& e) {
+            for (const auto& d : e.diagnostics()) failures.push_back(d);
+        }
+    }
+    if (!failures.empty()) throw CompileError(std::move(failures));
+    std::lock_guard lk(mu_);
+    make_current();
+    std::vector<CompiledKernel> out;
+    for (const nvrtc::Unit& u : built) {
+        cudaLibrary_t lib = nullptr;
+        cudaError_t e = cudaLibraryLoadData(&lib, u.cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            throw CompileError({{u.unit_name, std::string("cubin load failed: ") + cudaGetErrorString(e)}});
+        }
+        jit_libs_.push_back(lib);
+        const std::string tag = "nvrtc#" + std::to_string(++jit_units_) + ":" + u.unit_name;
+        for (const std::string& name : u.kernels) {
+            cudaKernel_t k = nullptr;
+            e = cudaLibraryGetKernel(&k, lib, ("hetreco_entry_" + name).c_str());
+            if (e != cudaSuccess) {
+                cudaGetLastError();
+                throw CompileError({{u.unit_name, "entry point for kernel '" + name + "' missing from the cubin"}});
+            }
+            jit_[tag + "/" + name] = k;
+            out.push_back({name, tag, &device_only_entry});
+        }
+    }
+    return out;
 }
 
 void* CudaBackend::stage_params(std::span<const std::byte> params) {
@@ -207,8 +250,14 @@ void* CudaBackend::stage_params(std::span<const std::byte> params) {
 
 void CudaBackend::execute(const CompiledKernel& kernel, const KernelBinding& bind, std::uint64_t gsize) {
     std::lock_guard lk(mu_);
-    const int which = dev::builtin_from_name(kernel.name.c_str());
-    if (which < 0) throw DeviceError(kernel.name, "no sm_100a implementation registered under this name");
+    cudaKernel_t jit = nullptr;
+    if (kernel.unit_name.rfind("nvrtc#", 0) == 0) {
+        auto it = jit_.find(kernel.unit_name + "/" + kernel.name);
+        if (it == jit_.end()) throw DeviceError(kernel.name, "kernel was compiled by another backend");
+        jit = it->second;
+    }
+    const int which = jit ? -1 : dev::builtin_from_name(kernel.name.c_str());
+    if (!jit && which < 0) throw DeviceError(kernel.name, "no sm_100a implementation registered under this name");
     hetreco_kernel_args args{};
     args.in = lookup(bind.input).ptr;
     args.in_layout = static_cast<const std::uint64_t*>(lookup(bind.input_header).ptr);
@@ -218,7 +267,18 @@ void CudaBackend::execute(const CompiledKernel& kernel, const KernelBinding& bin
     args.params = stage_params(bind.params);
     args.params_size = bind.params.size();
     last_kernel_ = kernel.name;
-    const cudaError_t e = dev::launch_builtin(dev::Builtin(which), args, gsize, compute_);
+    cudaError_t e;
+    if (jit) {
+        // grid-stride entry: enough CTAs to fill the GPU, never more than needed
+        int sms = 148;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ordinal_);
+        const std::uint64_t blocks = std::min<std::uint64_t>((gsize + 255) / 256, std::uint64_t(sms) * 16);
+        void* kargs[] = {&args, &gsize};
+        e = cudaLaunchKernel(reinterpret_cast<const void*>(jit), dim3(unsigned(blocks ? blocks : 1)), dim3(256), kargs, 0,
+                             compute_);
+    } else {
+        e = dev::launch_builtin(dev::Builtin(which), args, gsize, compute_);
+    }
     if (e != cudaSuccess) throw DeviceError(kernel.name, cudaGetErrorString(e));
 }
 

@@ -87,7 +87,7 @@ EXPORTED = [
     "hetreco_session_timer_start", "hetreco_session_timer_stop",
     "hetreco_mat_read", "hetreco_mat_parse", "hetreco_image_read", "hetreco_raw_read", "hetreco_mat_count",
     "hetreco_mat_variable", "hetreco_mat_free", "hetreco_mat_write", "hetreco_image_write", "hetreco_raw_write",
-    "hetreco_gen_phantom", "hetreco_phantom_blobs",
+    "hetreco_gen_phantom", "hetreco_phantom_blobs", "hetreco_nvrtc_compile_check", "hetreco_nvrtc_available",
 ]
 
 
@@ -149,6 +149,7 @@ def lib():
         "hetreco_image_write": ([pc, vp], i32), "hetreco_raw_write": ([pc, pc, vp], i32),
         "hetreco_gen_phantom": ([vp, u64, u64, u64, u64, u64, vp, vp, vp], i32),
         "hetreco_phantom_blobs": ([u64, u64, u64, vp], i32),
+        "hetreco_nvrtc_compile_check": ([pc, pc, vp, u64, vp, u64], i32), "hetreco_nvrtc_available": ([vp], i32),
     })
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -859,3 +860,26 @@ def phantom_blobs(nx: int, ny: int, seed: int):
     out = (C.c_double * 12)()
     _ck(lib().hetreco_phantom_blobs(nx, ny, seed, out))
     return [tuple(out[4 * i: 4 * i + 4]) for i in range(3)]
+
+
+# ---------------------------------------------------------------------------
+# source kernels (NVRTC, sm_100a)
+# ---------------------------------------------------------------------------
+
+
+def nvrtc_available() -> bool:
+    v = C.c_int()
+    _ck(lib().hetreco_nvrtc_available(C.byref(v)))
+    return bool(v.value)
+
+
+def compile_check(unit_name: str, source: str):
+    """Compile one kernel-source unit for sm_100a without a device; returns
+    (kernel names, compiler log).  Raises CompileError with the log."""
+    names = C.create_string_buffer(4096)
+    log = C.create_string_buffer(65536)
+    rc = lib().hetreco_nvrtc_compile_check(unit_name.encode(), source.encode(), names, 4096, log, 65536)
+    if rc != 0:
+        msg = lib().hetreco_last_error().decode(errors="replace")
+        raise ERRORS.get(rc, HetrecoError)(msg)
+    return [n for n in names.value.decode().split("\n") if n], log.value.decode(errors="replace")

@@ -57,6 +57,23 @@ def test_cli_usage_errors_and_devices(tmp_path):
     assert r.returncode != 0 and "missing.pgm" in r.stderr
 
 
+def test_cli_compile_surfaces_log(tmp_path):
+    """A deliberately broken unit: CompileError whose log reaches the CLI's
+    exit message verbatim."""
+    if not h.nvrtc_available():
+        pytest.skip("libnvrtc not available")
+    good = tmp_path / "good.cl.src"
+    good.write_text("HETRECO_KERNEL(twice) { (void)gsize; float* o = (float*)hetreco_array_out(args, 0);"
+                    " o[gid] = 2.0f * ((const float*)hetreco_array_in(args, 0))[gid]; }\n")
+    r = run_cli("compile", "--source", good)
+    assert r.returncode == 0 and "good.cl.src: twice" in r.stdout
+    bad = tmp_path / "bad.cl.src"
+    bad.write_text("HETRECO_KERNEL(bad) {\n  undeclared_thing = 1;\n}\n")
+    r = run_cli("compile", "--source", good, "--source", bad, check=False)
+    assert r.returncode == 4
+    assert "bad.cl.src(2): error" in r.stderr and "undeclared_thing" in r.stderr
+
+
 # ---- GPU ---------------------------------------------------------------------------------
 
 @pytest.fixture(scope="module")
