@@ -91,6 +91,18 @@ int hetreco_cuda_execute(hetreco_cuda_backend b, const char* kernel_name, uint64
                          uint64_t global_size);
 /* Backend::synchronize (backend.hpp:78); surfaces device faults */
 int hetreco_cuda_synchronize(hetreco_cuda_backend b);
+/* supports_source_kernels (backend.hpp:51): 1 when NVRTC is available */
+int hetreco_cuda_supports_source(hetreco_cuda_backend b, int* yes);
+/* compile (backend.hpp:71): kernel-source units -> NVRTC sm_100a cubins,
+ * loaded into this backend.  out = one "unit_tag\tkernel_name\n" line per
+ * kernel (unit_tag identifies the compiled unit for execute_unit).
+ * CompileError carries the units' compiler logs. */
+int hetreco_cuda_compile(hetreco_cuda_backend b, int count, const char* const* unit_names, const char* const* sources,
+                         char* out, uint64_t cap);
+/* execute (backend.hpp:74-75) of a kernel returned by hetreco_cuda_compile */
+int hetreco_cuda_execute_unit(hetreco_cuda_backend b, const char* unit_tag, const char* kernel_name, uint64_t input,
+                              uint64_t input_header, uint64_t output, uint64_t output_header, const void* params,
+                              uint64_t params_size, uint64_t global_size);
 /* Page-locked host memory for full-rate DMA (the paper's pinned buffers). */
 int hetreco_host_alloc(uint64_t bytes, void** out);
 int hetreco_host_free(void* p);

@@ -51,7 +51,10 @@ void device_only(const hetreco_kernel_args*, std::uint64_t, std::uint64_t) {
 
 class CudaBackend final : public Backend {
 public:
-    explicit CudaBackend(int ordinal, std::uint64_t capacity = 0) {
+    // source_kernels: report supports_source_kernels() when NVRTC is present,
+    // so the reference session's load_builtin_kernels compiles its embedded
+    // sources for sm_100a (session.cpp:139-148); false = precompiled builtins.
+    explicit CudaBackend(int ordinal, std::uint64_t capacity = 0, bool source_kernels = true) {
         ck(hetreco_cuda_backend_create(ordinal, capacity, &h_));
         hetreco_device_desc d{};
         ck(hetreco_cuda_backend_device(h_, &d));
@@ -64,14 +67,16 @@ public:
         desc_.api_version = d.api_version;
         desc_.global_memory_bytes = d.global_memory_bytes;
         desc_.base_alignment_bytes = d.base_alignment_bytes;
-        desc_.supports_source_kernels = false;
+        int src = 0;
+        ck(hetreco_cuda_supports_source(h_, &src));
+        desc_.supports_source_kernels = source_kernels && src != 0;
     }
     ~CudaBackend() override { hetreco_cuda_backend_destroy(h_); }
 
     std::string_view id() const override { return id_; }
     std::vector<DeviceDescriptor> devices() const override { return {desc_}; }
     TransferPath transfer_path() const override { return TransferPath::Staged; }
-    bool supports_source_kernels() const override { return false; }
+    bool supports_source_kernels() const override { return desc_.supports_source_kernels; }
 
     BufferId allocate(std::uint64_t bytes) override {
         std::uint64_t id = 0;
@@ -98,10 +103,45 @@ public:
         }
         return ks;
     }
-    std::vector<CompiledKernel> compile(std::span<const ProgramSource>) override {
-        throw UnsupportedSource("backend '" + id_ + "' runs precompiled sm_100a kernels");
+    // Source units are compiled by NVRTC for sm_100a inside the B200 library
+    // (the role cpujit_backend.cpp:121-177 plays on the CPU); one call per
+    // unit so a failure reports that unit's own log.
+    std::vector<CompiledKernel> compile(std::span<const ProgramSource> units) override {
+        if (!desc_.supports_source_kernels)
+            throw UnsupportedSource("backend '" + id_ + "': NVRTC is not available");
+        std::vector<CompiledKernel> out;
+        std::vector<BuildDiagnostic> failures;
+        for (const ProgramSource& u : units) {
+            const char* name = u.unit_name.c_str();
+            const char* text = u.source_text.c_str();
+            std::string listing(1 << 16, '\0');
+            const int rc = hetreco_cuda_compile(h_, 1, &name, &text, listing.data(), listing.size());
+            if (rc != HETRECO_OK) {
+                // keep the unit's own compiler log (drop the library's header line)
+                std::string log = hetreco_last_error();
+                const std::string head = "--- unit '" + u.unit_name + "' ---\n";
+                if (const std::size_t at = log.find(head); at != std::string::npos) log = log.substr(at + head.size());
+                failures.push_back({u.unit_name, log});
+                continue;
+            }
+            listing.resize(std::strlen(listing.c_str()));
+            std::size_t at = 0;
+            while (at < listing.size()) {
+                const std::size_t tab = listing.find('\t', at), nl = listing.find('\n', at);
+                out.push_back({listing.substr(tab + 1, nl - tab - 1), listing.substr(at, tab - at), &device_only});
+                at = nl + 1;
+            }
+        }
+        if (!failures.empty()) throw CompileError(std::move(failures));
+        return out;
     }
     void execute(const CompiledKernel& k, const KernelBinding& b, std::uint64_t gsize) override {
+        if (k.unit_name.rfind("nvrtc#", 0) == 0) {
+            ck(hetreco_cuda_execute_unit(h_, k.unit_name.c_str(), k.name.c_str(), b.input, b.input_header, b.output,
+                                         b.output_header, b.params.data(), b.params.size(), gsize),
+               k.name);
+            return;
+        }
         ck(hetreco_cuda_execute(h_, k.name.c_str(), b.input, b.input_header, b.output, b.output_header,
                                 b.params.data(), b.params.size(), gsize),
            k.name);
@@ -123,8 +163,8 @@ std::vector<std::unique_ptr<Backend>> make_cuda_backends() {
     return v;
 }
 
-std::unique_ptr<Backend> make_cuda_backend(int ordinal, std::uint64_t capacity) {
-    return std::make_unique<CudaBackend>(ordinal, capacity);
+std::unique_ptr<Backend> make_cuda_backend(int ordinal, std::uint64_t capacity, bool source_kernels) {
+    return std::make_unique<CudaBackend>(ordinal, capacity, source_kernels);
 }
 
 }  // namespace hetreco_b200_integration

@@ -124,6 +124,7 @@ class _RefOnB200:
         L.refcuda_fft2d.argtypes = [_vp, _vp, _u64, _u64, _u64, _i32]
         L.refcuda_recon.argtypes = [_i32, _vp, _vp, _vp, _u64, _u64, _u64, _u64, _i32, C.POINTER(_f64),
                                     C.POINTER(_f64)]
+        L.refcuda_set_source_mode.argtypes = [_i32]
         self.L = L
 
     def __getattr__(self, name):  # refdrv_x -> refcuda_x
@@ -137,9 +138,13 @@ def ref_on_b200_available() -> bool:
     return os.path.exists(REF_ON_B200_SO)
 
 
-def use_reference_on_b200():
+def use_reference_on_b200(source_kernels: bool = False):
     """Context in which the ref_* helpers below run the reference's session
-    code on the B200 (integration adapter) instead of its CPU backend."""
+    code on the B200 (integration adapter) instead of its CPU backend.
+    source_kernels=True: the adapter reports source support, so the
+    reference's load_builtin_kernels compiles its embedded kernel sources with
+    NVRTC for sm_100a (session.cpp:139-148) instead of using the precompiled
+    builtins."""
     import contextlib
 
     @contextlib.contextmanager
@@ -149,9 +154,13 @@ def use_reference_on_b200():
         if _ref_b200 is None:
             _ref_b200 = _RefOnB200()
         _ref = _ref_b200
+        got = _ref_b200.L.refcuda_set_source_mode(1 if source_kernels else 0)
+        if source_kernels and not got:
+            raise RuntimeError("B200 adapter has no source-kernel support (NVRTC missing)")
         try:
             yield
         finally:
+            _ref_b200.L.refcuda_set_source_mode(0)
             _ref = saved
     return ctx()
 

@@ -29,7 +29,7 @@
 #ifdef HETRECO_REF_ON_B200
 #define REFDRV(name) refcuda_##name
 namespace hetreco_b200_integration {
-std::unique_ptr<hetreco::Backend> make_cuda_backend(int ordinal, std::uint64_t capacity);
+std::unique_ptr<hetreco::Backend> make_cuda_backend(int ordinal, std::uint64_t capacity, bool source_kernels);
 }
 #else
 #define REFDRV(name) refdrv_##name
@@ -45,13 +45,20 @@ thread_local std::string g_err;
 
 // Process-lifetime backend, deliberately leaked (no static destructor runs
 // after the CUDA runtime has torn itself down at exit).
+int g_source_mode = 0;  // B200 adapter: 1 = builtins compiled from the reference's sources by NVRTC
+
 std::unique_ptr<Backend>& backend() {
 #ifdef HETRECO_REF_ON_B200
-    static auto* b = new std::unique_ptr<Backend>(hetreco_b200_integration::make_cuda_backend(0, 0));
+    static auto* pre = new std::unique_ptr<Backend>(hetreco_b200_integration::make_cuda_backend(0, 0, false));
+    if (g_source_mode) {
+        static auto* src = new std::unique_ptr<Backend>(hetreco_b200_integration::make_cuda_backend(0, 0, true));
+        return *src;
+    }
+    return *pre;
 #else
     static auto* b = new std::unique_ptr<Backend>(make_reference_backend());
-#endif
     return *b;
+#endif
 }
 
 std::vector<std::byte> fft_params(uint32_t mode, uint64_t L, uint64_t S, uint64_t m, float scale,
@@ -339,5 +346,18 @@ int REFDRV(layout_header)(int count, const int* types, const int* ranks, const u
 int REFDRV(builtin_source_count)() { return int(builtin_kernel_sources().size()); }
 const char* REFDRV(builtin_source_name)(int i) { return builtin_kernel_sources()[std::size_t(i)].unit_name.c_str(); }
 const char* REFDRV(builtin_source_text)(int i) { return builtin_kernel_sources()[std::size_t(i)].source_text.c_str(); }
+
+// Selects the adapter flavour used by the following calls (B200 build only):
+// 0 = precompiled sm_100a builtins, 1 = the reference's embedded sources
+// compiled by NVRTC through Backend::compile.  Returns the backend's
+// supports_source_kernels().
+int REFDRV(set_source_mode)(int mode) {
+#ifdef HETRECO_REF_ON_B200
+    g_source_mode = mode;
+#else
+    (void)mode;
+#endif
+    return backend()->supports_source_kernels() ? 1 : 0;
+}
 
 }  // extern "C"

@@ -255,6 +255,48 @@ int hetreco_cuda_execute(hetreco_cuda_backend b, const char* name, uint64_t in, 
     });
 }
 
+int hetreco_cuda_supports_source(hetreco_cuda_backend b, int* yes) {
+    return guard([&] {
+        need(yes, "yes");
+        *yes = B(b).supports_source_kernels() ? 1 : 0;
+    });
+}
+
+int hetreco_cuda_compile(hetreco_cuda_backend b, int count, const char* const* unit_names, const char* const* sources,
+                         char* out, uint64_t cap) {
+    return guard([&] {
+        if (count < 0) throw InvalidArgument("count must be >= 0");
+        std::vector<ProgramSource> units;
+        for (int i = 0; i < count; ++i) {
+            need(unit_names, "unit_names");
+            need(unit_names[i], "unit name");
+            need(sources, "sources");
+            need(sources[i], "unit source");
+            units.push_back({unit_names[i], sources[i]});
+        }
+        std::string listing;
+        for (const CompiledKernel& k : B(b).compile(units)) listing += k.unit_name + "\t" + k.name + "\n";
+        if (out && cap) {
+            if (listing.size() + 1 > cap) throw InvalidArgument("kernel listing needs " + std::to_string(listing.size() + 1) + " bytes");
+            copy_str(out, cap, listing);
+        }
+    });
+}
+
+int hetreco_cuda_execute_unit(hetreco_cuda_backend b, const char* unit_tag, const char* name, uint64_t in,
+                              uint64_t inh, uint64_t out, uint64_t outh, const void* params, uint64_t psize,
+                              uint64_t gsize) {
+    return guard([&] {
+        need(unit_tag, "unit_tag");
+        need(name, "kernel_name");
+        if (gsize == 0) throw InvalidArgument(std::string("launch of kernel '") + name + "' with empty index space");
+        CompiledKernel k{name, unit_tag, nullptr};
+        KernelBinding bind{in, inh, out, outh,
+                           std::span<const std::byte>(static_cast<const std::byte*>(params), psize)};
+        B(b).execute(k, bind, gsize);
+    });
+}
+
 int hetreco_cuda_synchronize(hetreco_cuda_backend b) {
     return guard([&] { B(b).synchronize(); });
 }

@@ -88,6 +88,7 @@ EXPORTED = [
     "hetreco_mat_read", "hetreco_mat_parse", "hetreco_image_read", "hetreco_raw_read", "hetreco_mat_count",
     "hetreco_mat_variable", "hetreco_mat_free", "hetreco_mat_write", "hetreco_image_write", "hetreco_raw_write",
     "hetreco_gen_phantom", "hetreco_phantom_blobs", "hetreco_nvrtc_compile_check", "hetreco_nvrtc_available",
+    "hetreco_cuda_supports_source", "hetreco_cuda_compile", "hetreco_cuda_execute_unit",
 ]
 
 
@@ -150,6 +151,8 @@ def lib():
         "hetreco_gen_phantom": ([vp, u64, u64, u64, u64, u64, vp, vp, vp], i32),
         "hetreco_phantom_blobs": ([u64, u64, u64, vp], i32),
         "hetreco_nvrtc_compile_check": ([pc, pc, vp, u64, vp, u64], i32), "hetreco_nvrtc_available": ([vp], i32),
+        "hetreco_cuda_supports_source": ([vp, vp], i32), "hetreco_cuda_compile": ([vp, i32, vp, vp, vp, u64], i32),
+        "hetreco_cuda_execute_unit": ([vp, pc, pc, u64, u64, u64, u64, vp, u64, u64], i32),
     })
     for name, (args, res) in sig.items():
         f = getattr(L, name)

@@ -3,7 +3,12 @@ layout.cpp, kernels.cpp ... compiled from /root/reference into oracle/_ref)
 runs on the B200 through the maintainer-side adapter
 integration/reference_cuda_backend.cpp over libhetreco_b200.so's C-ABI, and
 produces results BIT-IDENTICAL to the same code on the reference CPU backend:
-the builtin kernels reproduce the reference rounding exactly."""
+the builtin kernels reproduce the reference rounding exactly.
+
+Every test runs twice on the B200: with the precompiled sm_100a builtins,
+and with the adapter reporting source support, in which case the reference's
+own ComputeSession::load_builtin_kernels compiles its embedded kernel
+sources through Backend::compile -> NVRTC (SURVEY.md §8 f.4)."""
 import struct
 
 import numpy as np
@@ -25,35 +30,40 @@ def cplx(rng, *shape):
     return np.asfortranarray((rng.standard_normal(shape) + 1j * rng.standard_normal(shape)).astype(np.complex64))
 
 
-def both(fn):
+@pytest.fixture(params=[False, True], ids=["precompiled", "nvrtc-sources"])
+def source_mode(request):
+    return request.param
+
+
+def both(fn, source=False):
     cpu = fn()
-    with o.use_reference_on_b200():
+    with o.use_reference_on_b200(source):
         gpu = fn()
     return cpu, gpu
 
 
-def test_reference_session_on_b200_negate():
+def test_reference_session_on_b200_negate(source_mode):
     rng = np.random.default_rng(0)
     x = rng.integers(0, 256, 100003).astype(np.uint8)
-    cpu, gpu = both(lambda: o.ref_run_kernel("negate", x, struct.pack("<d", 200.0), x.size))
+    cpu, gpu = both(lambda: o.ref_run_kernel("negate", x, struct.pack("<d", 200.0), x.size), source_mode)
     assert beq(cpu, gpu)
     f = rng.random(4099).astype(np.float32)
-    cpu, gpu = both(lambda: o.ref_run_kernel("negate", f, struct.pack("<d", 1.0), f.size))
+    cpu, gpu = both(lambda: o.ref_run_kernel("negate", f, struct.pack("<d", 1.0), f.size), source_mode)
     assert beq(cpu, gpu)
 
 
 @pytest.mark.parametrize("shape", [(16, 8, 3), (64, 32, 2), (256, 256, 4)])
-def test_reference_fft_plan_on_b200_bitexact(shape):
+def test_reference_fft_plan_on_b200_bitexact(shape, source_mode):
     x = cplx(np.random.default_rng(sum(shape)), *shape)
     for inverse in (True, False):
-        cpu, gpu = both(lambda: o.ref_fft2d(x, inverse))
+        cpu, gpu = both(lambda: o.ref_fft2d(x, inverse), source_mode)
         assert beq(cpu, gpu)
 
 
 @pytest.mark.parametrize("method", ["sens", "rss"])
-def test_reference_recon_chain_on_b200_bitexact(method):
+def test_reference_recon_chain_on_b200_bitexact(method, source_mode):
     rng = np.random.default_rng(4)
     Y = cplx(rng, 128, 64, 8, 3)
     S = cplx(rng, 128, 64, 8) if method == "sens" else None
-    cpu, gpu = both(lambda: o.ref_recon(method, Y, S)[0])
+    cpu, gpu = both(lambda: o.ref_recon(method, Y, S)[0], source_mode)
     assert beq(cpu, gpu)
