@@ -29,7 +29,7 @@
 // the result is deterministic for a given K.
 //
 // Arithmetic per coil image is exactly the two-pass kernels' (same LineFFT
-// plan and twiddles, same product rounding, fp32 coil-ordered accumulation),
+// plan and twiddles, same fused fp32 coil-ordered accumulation),
 // so outputs are bit-identical to them except where a frame is split.
 // Reference semantics: complex_element_prod.cl.src:9-19 (conj product),
 // ximage_sum.cl.src:6-23 (coil sum), rss_combine.cl.src:5-20 (RSS),
@@ -302,21 +302,9 @@ __global__ void __launch_bounds__(Geo<kCL>::threads, Geo<kCL>::min_blocks)
         __syncthreads();
         cluster_arrive_relaxed();
         if constexpr (SENSE) {
-            sfor<R>([&](auto m) {
-                const float2 xv = v[m.value];
-                const float2 s = sv[m.value];
-                // x * conj(s) with the reference's rounding (kernel_abi.h:123-125)
-                const float nsi = -s.y;
-                const float re = __fsub_rn(__fmul_rn(xv.x, s.x), __fmul_rn(xv.y, nsi));
-                const float im = __fadd_rn(__fmul_rn(xv.x, nsi), __fmul_rn(xv.y, s.x));
-                acc_re[m.value] = __fadd_rn(acc_re[m.value], re);
-                acc_im[m.value] = __fadd_rn(acc_im[m.value], im);
-            });
+            sfor<R>([&](auto m) { mac_conj(acc_re[m.value], acc_im[m.value], v[m.value], sv[m.value]); });
         } else {
-            sfor<R>([&](auto m) {
-                const float2 xv = v[m.value];
-                acc_re[m.value] = __fadd_rn(acc_re[m.value], __fadd_rn(__fmul_rn(xv.x, xv.x), __fmul_rn(xv.y, xv.y)));
-            });
+            sfor<R>([&](auto m) { mac_abs2(acc_re[m.value], v[m.value]); });
         }
         if (c + 1 == C || w + 1 == w1) {
             finish_frame(f);

@@ -74,6 +74,16 @@ __device__ __forceinline__ float2 cmul(float2 a, float2 b) {
 }
 __device__ __forceinline__ float2 cscale(float2 a, float s) { return make_float2(a.x * s, a.y * s); }
 
+// fp32 coil-combine accumulation, products fused into the sums (4 FFMA per
+// sample instead of 4 FMUL + 4 FADD).  acc += x * conj(s)  /  acc += |x|^2.
+// The fp64 combine variants keep the reference's separately rounded products
+// (complex_element_prod.cl.src + ximage_sum.cl.src) instead.
+__device__ __forceinline__ void mac_conj(float& re, float& im, float2 x, float2 s) {
+    re = fmaf(x.x, s.x, fmaf(x.y, s.y, re));
+    im = fmaf(x.y, s.x, fmaf(-x.x, s.y, im));
+}
+__device__ __forceinline__ void mac_abs2(float& acc, float2 x) { acc = fmaf(x.x, x.x, fmaf(x.y, x.y, acc)); }
+
 // v * W_N^K with W_N = exp(DIR * 2 pi i / N), N | 64, all at compile time.
 template <int N, int K, int DIR>
 __device__ __forceinline__ float2 wmul(float2 v) {

@@ -217,14 +217,13 @@ __global__ void __launch_bounds__(MINB > 1 ? 128 : 256, MINB > 1 ? MINB : 0) k_f
                 sfor<R>([&](auto m) {
                     const float2 xv = x[m.value];
                     const float2 s = sv[m.value];
-                    // x * conj(s) with the reference's rounding (kernel_abi.h:123-125)
-                    const float nsi = -s.y;
-                    const float re = __fsub_rn(__fmul_rn(xv.x, s.x), __fmul_rn(xv.y, nsi));
-                    const float im = __fadd_rn(__fmul_rn(xv.x, nsi), __fmul_rn(xv.y, s.x));
                     if constexpr (ACCF) {
-                        acc_re[m.value] = __fadd_rn(acc_re[m.value], re);
-                        acc_im[m.value] = __fadd_rn(acc_im[m.value], im);
+                        mac_conj(acc_re[m.value], acc_im[m.value], xv, s);
                     } else {
+                        // x * conj(s) with the reference's rounding (kernel_abi.h:123-125)
+                        const float nsi = -s.y;
+                        const float re = __fsub_rn(__fmul_rn(xv.x, s.x), __fmul_rn(xv.y, nsi));
+                        const float im = __fadd_rn(__fmul_rn(xv.x, nsi), __fmul_rn(xv.y, s.x));
                         acc_re[m.value] = __dadd_rn(acc_re[m.value], double(re));
                         acc_im[m.value] = __dadd_rn(acc_im[m.value], double(im));
                     }
@@ -233,8 +232,7 @@ __global__ void __launch_bounds__(MINB > 1 ? 128 : 256, MINB > 1 ? MINB : 0) k_f
                 sfor<R>([&](auto m) {
                     const float2 xv = x[m.value];
                     if constexpr (ACCF) {
-                        acc_re[m.value] =
-                            __fadd_rn(acc_re[m.value], __fadd_rn(__fmul_rn(xv.x, xv.x), __fmul_rn(xv.y, xv.y)));
+                        mac_abs2(acc_re[m.value], xv);
                     } else {
                         const double re = xv.x, im = xv.y;
                         acc_re[m.value] =

@@ -116,8 +116,9 @@ def test_backend_capacity_and_ranges():
 def test_builtin_registry(s):
     assert set(s.kernel_names()) == {"negate", "fft_radix2_pass", "complex_element_prod", "ximage_sum",
                                      "rss_combine", "matrix_add"}
-    with pytest.raises(h.UnsupportedSource):
+    with pytest.raises(h.CompileError):  # source units go to NVRTC (tests/test_source_kernels.py)
         s.load_kernels([("broken.cl.src", "this is not a kernel")])
+    assert len(s.kernel_names()) == 6
     hd = s.register_data([np.zeros(4, np.float32)])
     with pytest.raises(h.UnknownKernel):
         s.launch_kernel("nonexistent", hd, hd, b"", 4)
