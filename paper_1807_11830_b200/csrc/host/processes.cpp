@@ -794,7 +794,17 @@ public:
         // prefetch form measured per size on B200: register copy at 256,
         // ping-pong (two-way unrolled) at 512 (profiles/round1_summary.md)
         if ((variant_ & 2) && !std::getenv("HETRECO_COMBINE_VARIANT") && nx_ != 512) variant_ |= 8;
-        plan_.s2 = dev::plan_contig(nx_, mode_, ny_ * chunk_, sm_count(ord), variant_);
+        // HETRECO_COMBINE_TMA=1: the TMA bulk-copy ring combine
+        // (fft_combine_tma.cu), fp32 only.  Measured slower than the register
+        // prefetch on B200 (profiles/round1_combine.md), so opt-in.
+        const char* tma_env = std::getenv("HETRECO_COMBINE_TMA");
+        tma_ = (variant_ & 1) && dev::combine_tma_supported(nx_) && tma_env && *tma_env == '1';
+        if (tma_) {
+            plan_.s2 = dev::plan_combine_tma(nx_, mode_, ny_, chunk_, sm_count(ord));
+            const std::uint64_t tail_f = nf_ % chunk_;
+            if (tail_f) tail_tma_ = dev::plan_combine_tma(nx_, mode_, ny_, tail_f, sm_count(ord));
+        }
+        if (!tma_) plan_.s2 = dev::plan_contig(nx_, mode_, ny_ * chunk_, sm_count(ord), variant_);
         const std::uint64_t tail = nf_ % chunk_;
         if (tail) {
             tail_s1_ = dev::plan_strided(ny_, nx_, nc_ * tail, sm_count(ord));
@@ -821,7 +831,10 @@ public:
             mark(s);
             dev::ContigArgs a2{scratch_.as<float2>(), static_cast<char*>(out_) + f0 * plane * out_elem, smap_, ny_,
                                nc_, fc, shift_, shift_, scale, plan_.tw_x.as<float2>()};
-            ck(dev::launch_contig(nx_, +1, mode_, a2, full ? plan_.s2 : tail_s2_, s), name() + "/axis0+combine");
+            if (tma_)
+                ck(dev::launch_combine_tma(nx_, mode_, a2, full ? plan_.s2 : tail_tma_, s), name() + "/axis0+combine");
+            else
+                ck(dev::launch_contig(nx_, +1, mode_, a2, full ? plan_.s2 : tail_s2_, s), name() + "/axis0+combine");
             mark(s);
         }
     }
@@ -837,6 +850,8 @@ private:
     DevMem scratch_;
     FftPlan plan_;
     dev::LaunchShape tail_s1_, tail_s2_;
+    bool tma_ = false;
+    dev::LaunchShape tail_tma_;
     bool cluster_ = false;
     dev::ClusterPlan cplan_;
     dev::ClusterMap cmap_{};

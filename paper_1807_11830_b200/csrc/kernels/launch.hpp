@@ -97,6 +97,15 @@ cudaError_t launch_strided(std::uint64_t N, int dir, const StridedArgs& a, const
 cudaError_t launch_contig(std::uint64_t N, int dir, Combine mode, const ContigArgs& a,
                           const LaunchShape& s, cudaStream_t stream);
 
+// ---- axis-0 + combine fed by a TMA bulk-copy ring (fft_combine_tma.cu) -----------
+// Same contract as launch_contig with mode Sense/Rss and fp32 accumulation;
+// a.in = X [N, ny, C, F].  HETRECO_TMA_STAGES (2|3|4|6, default 4) = tiles in
+// flight per CTA.
+bool combine_tma_supported(std::uint64_t N);
+LaunchShape plan_combine_tma(std::uint64_t N, Combine mode, std::uint64_t ny, std::uint64_t frames, int device_sms);
+cudaError_t launch_combine_tma(std::uint64_t N, Combine mode, const ContigArgs& a, const LaunchShape& s,
+                               cudaStream_t stream);
+
 // ---- single-pass cluster reconstruction (fft_cluster.cu) ------------------------
 //
 // IFFT2 + Sense/Rss combine of [256, 256, C, F] k-space in ONE kernel: an

@@ -570,3 +570,28 @@ def test_cluster_recon_rejects_unsupported(s):
         h.Process(s, "sens_recon").set_input(hin2).set_output(hout2).init({"algorithm": "cluster", "cluster_size": 4})
     with pytest.raises(h.InvalidParams):
         h.Process(s, "sens_recon").set_input(hin2).set_output(hout2).init({"algorithm": "fastest"})
+
+
+@pytest.mark.parametrize("stages", ["2", "4"])
+@pytest.mark.parametrize("nx,ny,nc,nf,shift", [(256, 256, 6, 5, False), (256, 4, 3, 2, True), (512, 64, 2, 3, False),
+                                               (160, 96, 4, 2, True)])
+def test_recon_tma_combine_vs_oracle(s, monkeypatch, stages, nx, ny, nc, nf, shift):
+    """Opt-in TMA bulk-copy ring combine (fft_combine_tma.cu), incl. partial
+    row groups (ny=4 < the 8 rows a CTA owns at 256) and mixed radix."""
+    monkeypatch.setenv("HETRECO_COMBINE_TMA", "1")
+    monkeypatch.setenv("HETRECO_TMA_STAGES", stages)
+    rng = np.random.default_rng(nx + ny + nc)
+    Y = cplx(rng, nx, ny, nc, nf)
+    S = cplx(rng, nx, ny, nc)
+    ax = (0, 1)
+    Yr = np.fft.ifftshift(Y, axes=ax) if shift else Y
+    Sr = np.fft.ifftshift(S, axes=ax) if shift else S
+    X = np.fft.ifft2(Yr.astype(np.complex128), axes=ax)
+    ref = (np.conj(Sr.astype(np.complex128))[..., None] * X).sum(axis=2)
+    rss = np.sqrt((np.abs(X) ** 2).sum(axis=2))
+    if shift:
+        ref, rss = np.fft.fftshift(ref, axes=ax), np.fft.fftshift(rss, axes=ax)
+    (M,), _ = run_process(s, "sens_recon", [Y, S], [((nx, ny, nf), np.complex64)], {"shift": shift})
+    assert relmax(M, ref) <= TOL
+    (R,), _ = run_process(s, "rss_recon", [Y], [((nx, ny, nf), np.float32)], {"shift": shift})
+    assert relmax(R, rss) <= TOL
