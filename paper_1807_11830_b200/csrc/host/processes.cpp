@@ -804,11 +804,18 @@ public:
             const std::uint64_t tail_f = nf_ % chunk_;
             if (tail_f) tail_tma_ = dev::plan_combine_tma(nx_, mode_, ny_, tail_f, sm_count(ord));
         }
-        if (!tma_) plan_.s2 = dev::plan_contig(nx_, mode_, ny_ * chunk_, sm_count(ord), variant_);
+        // small problems (few frames): coil-parallel combine, fp32 only
+        auto plan2 = [&](std::uint64_t frames) {
+            if ((variant_ & 1) && !std::getenv("HETRECO_COMBINE_VARIANT") &&
+                dev::combine_cp_preferred(nx_, ny_ * frames, nc_, sm_count(ord)))
+                return dev::plan_combine_cp(nx_, mode_, ny_ * frames, sm_count(ord));
+            return dev::plan_contig(nx_, mode_, ny_ * frames, sm_count(ord), variant_);
+        };
+        if (!tma_) plan_.s2 = plan2(chunk_);
         const std::uint64_t tail = nf_ % chunk_;
         if (tail) {
             tail_s1_ = dev::plan_strided(ny_, nx_, nc_ * tail, sm_count(ord));
-            tail_s2_ = dev::plan_contig(nx_, mode_, ny_ * tail, sm_count(ord), variant_);
+            tail_s2_ = plan2(tail);
         }
     }
     void record(cudaStream_t s) override {
@@ -918,7 +925,9 @@ public:
         if (normal_) {
             tw_inv_ = twiddle_table(nx_, +1);
             if (scratch_.size() != nx_ * ny_ * nc_ * nf_ * 8) scratch_ = DevMem(nx_ * ny_ * nc_ * nf_ * 8);
-            s_comb_ = dev::plan_contig(nx_, dev::Combine::Sense, ny_ * nf_, sms);
+            s_comb_ = dev::combine_cp_preferred(nx_, ny_ * nf_, nc_, sms)
+                          ? dev::plan_combine_cp(nx_, dev::Combine::Sense, ny_ * nf_, sms)
+                          : dev::plan_contig(nx_, dev::Combine::Sense, ny_ * nf_, sms);
         }
     }
     void record(cudaStream_t s) override {
@@ -1045,6 +1054,8 @@ StreamingRecon::StreamingRecon(ComputeSession& s, Method method, std::uint64_t n
     }
     m.scratch = DevMem(in_frame_bytes_ * chunk);
     m.plan.make(nx, ny, +1, coils * chunk, m.mode, ny * chunk, cb.ordinal());
+    if (dev::combine_cp_preferred(nx, ny * chunk, coils, sm_count(cb.ordinal())))
+        m.plan.s2 = dev::plan_combine_cp(nx, m.mode, ny * chunk, sm_count(cb.ordinal()));
 }
 
 StreamingRecon::~StreamingRecon() = default;
@@ -1075,7 +1086,8 @@ void StreamingRecon::run(const void* host_in, std::uint64_t frames, void* host_o
         dev::LaunchShape s1 = m.plan.s1, s2 = m.plan.s2;
         if (nf != chunk_) {
             s1 = dev::plan_strided(m.ny, m.nx, m.nc * nf, sms);
-            s2 = dev::plan_contig(m.nx, m.mode, m.ny * nf, sms);
+            s2 = dev::combine_cp_preferred(m.nx, m.ny * nf, m.nc, sms) ? dev::plan_combine_cp(m.nx, m.mode, m.ny * nf, sms)
+                                                                        : dev::plan_contig(m.nx, m.mode, m.ny * nf, sms);
         }
         dev::StridedArgs a1{m.ybuf[b].as<float2>(), m.scratch.as<float2>(), m.nx, m.nc * nf, m.shift, m.shift, 1.0f,
                             m.plan.tw_y.as<float2>()};

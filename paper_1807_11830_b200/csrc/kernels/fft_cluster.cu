@@ -258,7 +258,8 @@ __global__ void __launch_bounds__(Geo<kCL>::threads, Geo<kCL>::min_blocks)
         mbar_wait(bar, parity);
         parity ^= 1;
         float2 v[R];
-        slots<R>(sh, [&](auto m, auto ms) { v[m.value] = stg[(jA + T * ms.value) * kTX + l]; });
+        slots_ld<R>(sh, (long long)(R / 2) * T * kTX,
+                    [&](auto m, long long d) { v[m.value] = stg[(jA + T * m.value) * kTX + l + d]; });
         // the first exchange barrier inside run_f also retires every read of the tile
         L::template run_f<+1>(
             v, [&](auto pc, auto sc, auto qc) { return twA[L::template tw_index<pc.value, sc.value, qc.value>(jA)]; },
@@ -286,7 +287,7 @@ __global__ void __launch_bounds__(Geo<kCL>::threads, Geo<kCL>::min_blocks)
         float2 sv[SENSE ? R : 1];
         if constexpr (SENSE) {
             const float2* sp = a.smap + std::uint64_t(c) * N * N + pix;
-            slots<R>(sh, [&](auto m, auto ms) { sv[m.value] = __ldg(sp + T * ms.value); });
+            slots_ld<R>(sh, (long long)(R / 2) * T, [&](auto m, long long d) { sv[m.value] = __ldg(sp + T * m.value + d); });
         }
         mbar_wait(rbar0 + 8 * b, (rpar >> b) & 1u);
         rpar ^= 1u << b;

@@ -126,13 +126,13 @@ __global__ void __launch_bounds__(LPB * LineFFT<N>::T)
         float2 sv[SENSE ? R : 1];
         if constexpr (SENSE) {
             const float2* sp = a.smap + (std::uint64_t(c) * ny + y) * N + j;
-            slots<R>(sh_out, [&](auto m, auto ms) { sv[m.value] = __ldg(sp + T * ms.value); });
+            slots_ld<R>(sh_out, (long long)(R / 2) * T, [&](auto m, long long d) { sv[m.value] = __ldg(sp + T * m.value + d); });
         }
         const int slot = int(t % K);
         bar_wait(bars + 8 * slot, (t / K) & 1u);
         float2 v[R];
         const float2* src = ring + slot * TILE + (active ? l : 0) * N + j;
-        slots<R>(sh_in, [&](auto m, auto ms) { v[m.value] = src[T * ms.value]; });
+        slots_ld<R>(sh_in, (long long)(R / 2) * T, [&](auto m, long long d) { v[m.value] = src[T * m.value + d]; });
         __syncthreads();  // every thread holds its row: the slot can be refilled
         if (tid == 0) {
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");

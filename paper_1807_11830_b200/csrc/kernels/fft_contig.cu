@@ -73,6 +73,7 @@ cudaError_t launch_contig(std::uint64_t N, int dir, Combine mode, const ContigAr
     const std::uint32_t items = std::uint32_t(items64);
     if (mode != Combine::None) {
         if (dir < 0) return cudaErrorInvalidValue;
+        if (s.variant & 128) return launch_combine_cp(N, mode, a, s, st);
         return combine_launch(mode, N, s.variant, a, s, lpb, items, st);
     }
     switch (N) {

@@ -182,6 +182,18 @@ __device__ __forceinline__ void slots(bool rot, F&& fn) {
         sfor<R>([&](auto ms) { fn(ms, ms); });
 }
 
+// Loads for the same rotation as slots(), written as addresses: slot m reads
+// position m + R/2 (m < R/2) or m - R/2 (m >= R/2) when `rot`.  fn(m, d)
+// receives d = +-half (the element offset of half a line, or 0): the
+// destination register stays compile-time, only the address moves, so a
+// prefetching load never needs a data-dependent register permutation (which
+// would make the consumer wait for the load right where it is issued).
+template <int R, class F>
+__device__ __forceinline__ void slots_ld(bool rot, long long half, F&& fn) {
+    const long long d = rot ? half : 0;
+    sfor<R>([&](auto m) { fn(m, m.value < R / 2 ? d : -d); });
+}
+
 // ---- per-size plan ------------------------------------------------------------------------
 
 // Radix lists are derived from (N, R): R points per thread, passes of radix R

@@ -84,10 +84,16 @@ __global__ void __launch_bounds__(MINB > 1 ? 256 : 512, MINB > 1 ? MINB : 0) k_f
     };
     auto load = [&](std::uint64_t off, float2(&v)[R]) {
         const float2* src = a.in + off;
-        if constexpr (NXC > 0) {
+        if constexpr (NXC > 0 && !PFS) {
+            // consumed at once: duplicated code paths with immediate offsets
+            // beat a moving base under the MINB register cap (measured)
             slots<R>(sh_in, [&](auto m, auto ms) { v[m.value] = __ldcs(src + ms.value * T * NXC); });
+        } else if constexpr (NXC > 0) {
+            slots_ld<R>(sh_in, (long long)(R / 2) * T * NXC,
+                        [&](auto m, long long d) { v[m.value] = __ldcs(src + m.value * T * NXC + d); });
         } else {
-            slots<R>(sh_in, [&](auto m, auto ms) { v[m.value] = __ldcs(src + ms.value * step); });
+            slots_ld<R>(sh_in, (long long)(R / 2) * step,
+                        [&](auto m, long long d) { v[m.value] = __ldcs(src + std::uint64_t(m.value) * step + d); });
         }
     };
     auto store = [&](std::uint64_t off, float2(&v)[R]) {
@@ -149,7 +155,8 @@ __global__ void __launch_bounds__(256) k_fft_contig(ContigArgs a, int lpb, std::
         const bool active = item < items;
         float2 v[R];
         const float2* src = a.in + std::uint64_t(item) * N + j;
-        slots<R>(sh_in, [&](auto m, auto ms) { v[m.value] = active ? src[T * ms.value] : make_float2(0.f, 0.f); });
+        slots_ld<R>(sh_in, (long long)(R / 2) * T,
+                    [&](auto m, long long d) { v[m.value] = active ? src[T * m.value + d] : make_float2(0.f, 0.f); });
         L::template run<DIR>(v, tw, line, j, [] { line_sync<T>(); }, a.scale);
         float2* dst = static_cast<float2*>(a.out) + std::uint64_t(item) * N + j;
         if (active) slots<R>(sh_out, [&](auto m, auto ms) { dst[T * ms.value] = v[m.value]; });
@@ -194,11 +201,11 @@ __global__ void __launch_bounds__(MINB > 1 ? 128 : 256, MINB > 1 ? MINB : 0) k_f
         const float2* sbase = a.smap + std::uint64_t(y) * N + j;
         auto load_x = [&](std::uint32_t c, float2(&d)[R]) {
             const float2* src = xbase + c * coil_stride;
-            slots<R>(sh_in, [&](auto m, auto ms) { d[m.value] = __ldcs(src + T * ms.value); });
+            slots_ld<R>(sh_in, (long long)(R / 2) * T, [&](auto m, long long o) { d[m.value] = __ldcs(src + T * m.value + o); });
         };
         auto load_s = [&](std::uint32_t c, float2(&d)[R]) {
             const float2* src = sbase + c * coil_stride;
-            slots<R>(sh_out, [&](auto m, auto ms) { d[m.value] = __ldg(src + T * ms.value); });
+            slots_ld<R>(sh_out, (long long)(R / 2) * T, [&](auto m, long long o) { d[m.value] = __ldg(src + T * m.value + o); });
         };
         Acc acc_re[R], acc_im[R];
         sfor<R>([&](auto m) {

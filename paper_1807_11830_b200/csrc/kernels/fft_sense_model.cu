@@ -46,7 +46,9 @@ __global__ void __launch_bounds__(256) k_fft_expand(ContigArgs a, int lpb, std::
         const float2* mrow = a.in + (std::uint64_t(f) * ny + y) * N + j;
         const float2* srow = a.smap + (std::uint64_t(c) * ny + y) * N + j;
         float2 v[R];
-        slots<R>(sh_in, [&](auto m, auto ms) { v[m.value] = cmul_ref(__ldg(srow + T * ms.value), mrow[T * ms.value]); });
+        slots_ld<R>(sh_in, (long long)(R / 2) * T, [&](auto m, long long d) {
+            v[m.value] = cmul_ref(__ldg(srow + T * m.value + d), mrow[T * m.value + d]);
+        });
         L::template run<-1>(v, tw, line, j, [] { line_sync<T>(); }, 1.0f);
         float2* dst = static_cast<float2*>(a.out) + std::uint64_t(it) * N + j;
         if (active) slots<R>(sh_out, [&](auto m, auto ms) { dst[T * ms.value] = v[m.value]; });
@@ -75,7 +77,8 @@ __global__ void __launch_bounds__(256) k_fft_strided_masked(StridedArgs a, int t
         const std::uint64_t off = std::uint64_t(plane) * NX * N + col + std::uint32_t(j) * NX;
         const float2* src = a.in + off;
         float2 v[R];
-        slots<R>(sh_in, [&](auto m, auto ms) { v[m.value] = __ldcs(src + ms.value * T * NX); });
+        slots_ld<R>(sh_in, (long long)(R / 2) * T * NX,
+                    [&](auto m, long long d) { v[m.value] = __ldcs(src + m.value * T * NX + d); });
         L::template run<-1>(v, tw, line, j, [] { __syncthreads(); });
         // mask at the displayed k-space position (fftshift'ed when shifting)
         const float* mrow = a.mask ? a.mask + col + std::uint32_t(j) * NX : nullptr;

@@ -97,6 +97,15 @@ cudaError_t launch_strided(std::uint64_t N, int dir, const StridedArgs& a, const
 cudaError_t launch_contig(std::uint64_t N, int dir, Combine mode, const ContigArgs& a,
                           const LaunchShape& s, cudaStream_t stream);
 
+// ---- coil-parallel axis-0 + combine for small problems (fft_combine_cp.cu) -------
+// One CTA per output line, G coil groups transform coils in parallel and the
+// partials are summed in group order (fp32).  launch_contig dispatches a shape
+// from plan_combine_cp (variant bit 128) here.
+bool combine_cp_preferred(std::uint64_t N, std::uint64_t items /* ny*F */, std::uint64_t coils, int device_sms);
+LaunchShape plan_combine_cp(std::uint64_t N, Combine mode, std::uint64_t items, int device_sms);
+cudaError_t launch_combine_cp(std::uint64_t N, Combine mode, const ContigArgs& a, const LaunchShape& s,
+                              cudaStream_t stream);
+
 // ---- axis-0 + combine fed by a TMA bulk-copy ring (fft_combine_tma.cu) -----------
 // Same contract as launch_contig with mode Sense/Rss and fp32 accumulation;
 // a.in = X [N, ny, C, F].  HETRECO_TMA_STAGES (2|3|4|6, default 4) = tiles in

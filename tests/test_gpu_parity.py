@@ -531,13 +531,13 @@ def test_cluster_recon_relaunch_and_two_pass_agreement(s):
     """Counters self-reset: repeated launches give identical results; with
     whole frames per cluster the result is bit-identical to the two-pass chain
     (same per-coil arithmetic, same coil order)."""
-    nx, nc, nf = 256, 4, 6
+    nx, nc, nf = 256, 3, 12  # enough lines for the coil-serial combine (the coil-parallel one sums in another order)
     rng = np.random.default_rng(5)
     Y = cplx(rng, nx, nx, nc, nf)
     S = cplx(rng, nx, nx, nc)
     hin = s.register_data(h.Data([Y, S], h.DataKind.KData))
     outs = []
-    for prm in ({"algorithm": "cluster", "max_clusters": 5},        # frames split across clusters
+    for prm in ({"algorithm": "cluster", "max_clusters": 7},        # frames split across clusters
                 {"algorithm": "cluster", "max_clusters": nf},       # one frame per cluster
                 {"algorithm": "two_pass"}):
         hout = s.allocate_data([((nx, nx, nf), np.complex64)])
@@ -594,4 +594,26 @@ def test_recon_tma_combine_vs_oracle(s, monkeypatch, stages, nx, ny, nc, nf, shi
     (M,), _ = run_process(s, "sens_recon", [Y, S], [((nx, ny, nf), np.complex64)], {"shift": shift})
     assert relmax(M, ref) <= TOL
     (R,), _ = run_process(s, "rss_recon", [Y], [((nx, ny, nf), np.float32)], {"shift": shift})
+    assert relmax(R, rss) <= TOL
+
+
+@pytest.mark.parametrize("nx,nc,nf,shift", [(256, 8, 1, False), (256, 8, 2, True), (512, 5, 1, False), (160, 6, 1, True),
+                                           (64, 3, 4, False)])
+def test_coil_parallel_combine_small_problems(s, nx, nc, nf, shift):
+    """Few frames -> the coil-parallel combine (fft_combine_cp.cu): one CTA per
+    output line, coil groups in parallel, partials summed in group order."""
+    rng = np.random.default_rng(nx * nc + nf)
+    Y = cplx(rng, nx, nx, nc, nf)
+    S = cplx(rng, nx, nx, nc)
+    ax = (0, 1)
+    Yr = np.fft.ifftshift(Y, axes=ax) if shift else Y
+    Sr = np.fft.ifftshift(S, axes=ax) if shift else S
+    X = np.fft.ifft2(Yr.astype(np.complex128), axes=ax)
+    ref = (np.conj(Sr.astype(np.complex128))[..., None] * X).sum(axis=2)
+    rss = np.sqrt((np.abs(X) ** 2).sum(axis=2))
+    if shift:
+        ref, rss = np.fft.fftshift(ref, axes=ax), np.fft.fftshift(rss, axes=ax)
+    (M,), _ = run_process(s, "sens_recon", [Y, S], [((nx, nx, nf), np.complex64)], {"shift": shift})
+    assert relmax(M, ref) <= TOL
+    (R,), _ = run_process(s, "rss_recon", [Y], [((nx, nx, nf), np.float32)], {"shift": shift})
     assert relmax(R, rss) <= TOL
