@@ -25,6 +25,16 @@ void ck(cudaError_t e, const std::string& what) {
 
 bool is_pow2(std::uint64_t v) { return v && !(v & (v - 1)); }
 
+// The staged-map SENSE combine (fft_combine_ss.cu) where it measured faster
+// (256^2 C3: 131 -> 121 us; 512^2: 162 -> 202 us, 160^2: even), unless
+// HETRECO_COMBINE_SS=0 (off) / =1 (every supported size).
+bool combine_ss_enabled(std::uint64_t nx) {
+    const char* e = std::getenv("HETRECO_COMBINE_SS");
+    if (e && *e == '0') return false;
+    if (!dev::combine_ss_supported(nx)) return false;
+    return (e && *e == '1') || (nx >= 64 && nx <= 256 && is_pow2(nx));
+}
+
 // Owning device allocation on the session's GPU.
 class DevMem {
 public:
@@ -806,9 +816,12 @@ public:
         }
         // small problems (few frames): coil-parallel combine, fp32 only
         auto plan2 = [&](std::uint64_t frames) {
-            if ((variant_ & 1) && !std::getenv("HETRECO_COMBINE_VARIANT") &&
-                dev::combine_cp_preferred(nx_, ny_ * frames, nc_, sm_count(ord)))
-                return dev::plan_combine_cp(nx_, mode_, ny_ * frames, sm_count(ord));
+            if ((variant_ & 1) && !std::getenv("HETRECO_COMBINE_VARIANT")) {
+                if (dev::combine_cp_preferred(nx_, ny_ * frames, nc_, sm_count(ord)))
+                    return dev::plan_combine_cp(nx_, mode_, ny_ * frames, sm_count(ord));
+                if (mode_ == dev::Combine::Sense && combine_ss_enabled(nx_))
+                    return dev::plan_combine_ss(nx_, ny_, frames, sm_count(ord));
+            }
             return dev::plan_contig(nx_, mode_, ny_ * frames, sm_count(ord), variant_);
         };
         if (!tma_) plan_.s2 = plan2(chunk_);
@@ -927,7 +940,8 @@ public:
             if (scratch_.size() != nx_ * ny_ * nc_ * nf_ * 8) scratch_ = DevMem(nx_ * ny_ * nc_ * nf_ * 8);
             s_comb_ = dev::combine_cp_preferred(nx_, ny_ * nf_, nc_, sms)
                           ? dev::plan_combine_cp(nx_, dev::Combine::Sense, ny_ * nf_, sms)
-                          : dev::plan_contig(nx_, dev::Combine::Sense, ny_ * nf_, sms);
+                          : combine_ss_enabled(nx_) ? dev::plan_combine_ss(nx_, ny_, nf_, sms)
+                                                    : dev::plan_contig(nx_, dev::Combine::Sense, ny_ * nf_, sms);
         }
     }
     void record(cudaStream_t s) override {
@@ -1056,6 +1070,8 @@ StreamingRecon::StreamingRecon(ComputeSession& s, Method method, std::uint64_t n
     m.plan.make(nx, ny, +1, coils * chunk, m.mode, ny * chunk, cb.ordinal());
     if (dev::combine_cp_preferred(nx, ny * chunk, coils, sm_count(cb.ordinal())))
         m.plan.s2 = dev::plan_combine_cp(nx, m.mode, ny * chunk, sm_count(cb.ordinal()));
+    else if (m.mode == dev::Combine::Sense && combine_ss_enabled(nx))
+        m.plan.s2 = dev::plan_combine_ss(nx, ny, chunk, sm_count(cb.ordinal()));
 }
 
 StreamingRecon::~StreamingRecon() = default;
@@ -1087,7 +1103,8 @@ void StreamingRecon::run(const void* host_in, std::uint64_t frames, void* host_o
         if (nf != chunk_) {
             s1 = dev::plan_strided(m.ny, m.nx, m.nc * nf, sms);
             s2 = dev::combine_cp_preferred(m.nx, m.ny * nf, m.nc, sms) ? dev::plan_combine_cp(m.nx, m.mode, m.ny * nf, sms)
-                                                                        : dev::plan_contig(m.nx, m.mode, m.ny * nf, sms);
+                 : (m.mode == dev::Combine::Sense && combine_ss_enabled(m.nx)) ? dev::plan_combine_ss(m.nx, m.ny, nf, sms)
+                                                                              : dev::plan_contig(m.nx, m.mode, m.ny * nf, sms);
         }
         dev::StridedArgs a1{m.ybuf[b].as<float2>(), m.scratch.as<float2>(), m.nx, m.nc * nf, m.shift, m.shift, 1.0f,
                             m.plan.tw_y.as<float2>()};

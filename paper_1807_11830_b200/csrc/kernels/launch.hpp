@@ -106,6 +106,13 @@ LaunchShape plan_combine_cp(std::uint64_t N, Combine mode, std::uint64_t items, 
 cudaError_t launch_combine_cp(std::uint64_t N, Combine mode, const ContigArgs& a, const LaunchShape& s,
                               cudaStream_t stream);
 
+// ---- SENSE combine with the map row staged in shared memory (fft_combine_ss.cu) --
+// CTA = one row y of 8 consecutive frames sharing S[:, y, c]; fp32, SENSE only.
+// launch_contig dispatches a shape from plan_combine_ss (variant bit 256) here.
+bool combine_ss_supported(std::uint64_t N);
+LaunchShape plan_combine_ss(std::uint64_t N, std::uint64_t ny, std::uint64_t frames, int device_sms);
+cudaError_t launch_combine_ss(std::uint64_t N, const ContigArgs& a, const LaunchShape& s, cudaStream_t stream);
+
 // ---- axis-0 + combine fed by a TMA bulk-copy ring (fft_combine_tma.cu) -----------
 // Same contract as launch_contig with mode Sense/Rss and fp32 accumulation;
 // a.in = X [N, ny, C, F].  HETRECO_TMA_STAGES (2|3|4|6, default 4) = tiles in

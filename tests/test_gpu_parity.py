@@ -617,3 +617,26 @@ def test_coil_parallel_combine_small_problems(s, nx, nc, nf, shift):
     assert relmax(M, ref) <= TOL
     (R,), _ = run_process(s, "rss_recon", [Y], [((nx, nx, nf), np.float32)], {"shift": shift})
     assert relmax(R, rss) <= TOL
+
+
+@pytest.mark.parametrize("nx,ny,nc,nf,shift", [(256, 256, 5, 13, False), (256, 128, 3, 9, True), (512, 512, 2, 9, True),
+                                               (160, 160, 3, 17, False), (64, 32, 4, 20, True)])
+def test_staged_map_combine(s, monkeypatch, nx, ny, nc, nf, shift):
+    """SENSE combine with the map row staged in shared memory (fft_combine_ss.cu,
+    forced on for every size): frame groups with a partial tail, shift, mixed
+    radix; bit-identical to the register-prefetch combine."""
+    rng = np.random.default_rng(nx + nf)
+    Y = cplx(rng, nx, ny, nc, nf)
+    S = cplx(rng, nx, ny, nc)
+    monkeypatch.setenv("HETRECO_COMBINE_SS", "1")
+    (M,), _ = run_process(s, "sens_recon", [Y, S], [((nx, ny, nf), np.complex64)], {"shift": shift})
+    monkeypatch.setenv("HETRECO_COMBINE_SS", "0")
+    (M0,), _ = run_process(s, "sens_recon", [Y, S], [((nx, ny, nf), np.complex64)], {"shift": shift})
+    assert beq(M, M0)
+    ax = (0, 1)
+    Yr = np.fft.ifftshift(Y, axes=ax) if shift else Y
+    Sr = np.fft.ifftshift(S, axes=ax) if shift else S
+    ref = (np.conj(Sr.astype(np.complex128))[..., None] * np.fft.ifft2(Yr.astype(np.complex128), axes=ax)).sum(axis=2)
+    if shift:
+        ref = np.fft.fftshift(ref, axes=ax)
+    assert relmax(M, ref) <= TOL
