@@ -236,7 +236,8 @@ def run_ours(args):
     kernels = [
         {"name": "k_fft_strided<256,+1,256,16> (axis-1 IFFT, column tiles)", "seconds": k_axis1, "bytes": bytes_axis1,
          "gbs": bytes_axis1 / k_axis1 / 1e9},
-        {"name": "k_fft_combine<256,SENSE,fp32,prefetch> (axis-0 IFFT + conj(S) coil combine)", "seconds": k_axis0,
+        {"name": "k_fft_combine_ss<256,8> (axis-0 IFFT + conj(S) coil combine, map rows staged in smem)",
+         "seconds": k_axis0,
          "bytes": bytes_axis0, "gbs": bytes_axis0 / k_axis0 / 1e9},
     ]
     for k in kernels:
