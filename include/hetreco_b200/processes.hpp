@@ -139,6 +139,8 @@ protected:
     void capture();
     // Processes call mark(s) after each kernel they enqueue in record().
     void mark(cudaStream_t s);
+    // true while profile() replays record() kernel by kernel (no graph)
+    bool profiling() const { return profiling_; }
 
 private:
     ProcessParams params_;

@@ -25,6 +25,11 @@ void ck(cudaError_t e, const std::string& what) {
 
 bool is_pow2(std::uint64_t v) { return v && !(v & (v - 1)); }
 
+long env_or(const char* name, long fallback) {
+    const char* v = std::getenv(name);
+    return v && *v ? std::atol(v) : fallback;
+}
+
 // The staged-map SENSE combine (fft_combine_ss.cu) where it measured faster
 // (256^2 C3: 131 -> 121 us; 512^2: 162 -> 202 us, 160^2: even), unless
 // HETRECO_COMBINE_SS=0 (off) / =1 (every supported size).
@@ -720,7 +725,8 @@ public:
     ReconProcess(ComputeSession& s, std::string name, dev::Combine mode)
         : GraphProcess(s, std::move(name)), mode_(mode) {}
     void bake(const ProcessParams& p) override {
-        p.require_known({"shift", "chunk_frames", "accumulate", "prefetch", "algorithm", "max_clusters", "cluster_size"});
+        p.require_known({"shift", "chunk_frames", "accumulate", "prefetch", "algorithm", "max_clusters", "cluster_size",
+                         "overlap"});
         shift_ = p.get_bool("shift", false);
         const std::string acc = p.get_string("accumulate", "fp32");
         if (acc != "fp32" && acc != "fp64")
@@ -830,6 +836,32 @@ public:
             tail_s1_ = dev::plan_strided(ny_, nx_, nc_ * tail, sm_count(ord));
             tail_s2_ = plan2(tail);
         }
+        // "overlap": true -- pipeline over 8-frame chunks (one full-size
+        // intermediate): the axis-1 pass of chunk k+1 runs as a graph branch
+        // concurrent with the combine of chunk k (HBM-bound next to
+        // issue-bound).  Measured slower on B200 (C3: 337 vs 298 us; both
+        // kernels size their grids to fill every SM, so the branches contend
+        // instead of overlapping), hence off by default.
+        overlap_ = false;
+        std::int64_t oc = std::int64_t(env_or("HETRECO_OVERLAP_CHUNK", 8));
+        if (p.get_bool("overlap", false) && chunk_ == nf_ && !tma_ && oc > 0 && nf_ >= 2 * std::uint64_t(oc)) {
+            overlap_ = true;
+            ovl_chunk_ = std::uint64_t(oc);
+            const std::uint64_t ot = nf_ % ovl_chunk_;
+            ovl_s1_ = dev::plan_strided(ny_, nx_, nc_ * ovl_chunk_, sm_count(ord));
+            ovl_s2_ = plan2(ovl_chunk_);
+            if (ot) {
+                ovl_tail_s1_ = dev::plan_strided(ny_, nx_, nc_ * ot, sm_count(ord));
+                ovl_tail_s2_ = plan2(ot);
+            }
+            const std::size_t nchunks = std::size_t((nf_ + ovl_chunk_ - 1) / ovl_chunk_);
+            if (!side_) ck(cudaStreamCreateWithFlags(&side_, cudaStreamNonBlocking), "cudaStreamCreate(overlap)");
+            while (ovl_events_.size() < nchunks + 2) {
+                cudaEvent_t e = nullptr;
+                ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate(overlap)");
+                ovl_events_.push_back(e);
+            }
+        }
     }
     void record(cudaStream_t s) override {
         const float scale = float(1.0 / (double(nx_) * double(ny_)));
@@ -842,6 +874,32 @@ public:
         }
         const std::uint64_t plane = nx_ * ny_;
         const std::uint64_t out_elem = mode_ == dev::Combine::Sense ? 8 : 4;
+        if (overlap_ && !profiling()) {
+            // fork: the side stream joins the capture, runs the combines
+            cudaEvent_t* ev = ovl_events_.data();
+            ck(cudaEventRecord(ev[0], s), "overlap fork");
+            ck(cudaStreamWaitEvent(side_, ev[0], 0), "overlap fork");
+            std::size_t k = 0;
+            for (std::uint64_t f0 = 0; f0 < nf_; f0 += ovl_chunk_, ++k) {
+                const std::uint64_t fc = std::min(ovl_chunk_, nf_ - f0);
+                const bool full = fc == ovl_chunk_;
+                float2* x = scratch_.as<float2>() + f0 * plane * nc_;
+                dev::StridedArgs a1{y_ + f0 * plane * nc_, x, nx_, nc_ * fc, shift_, shift_, 1.0f,
+                                    plan_.tw_y.as<float2>()};
+                ck(dev::launch_strided(ny_, +1, a1, full ? ovl_s1_ : ovl_tail_s1_, s), name() + "/axis1");
+                ck(cudaEventRecord(ev[k + 1], s), "overlap edge");
+                ck(cudaStreamWaitEvent(side_, ev[k + 1], 0), "overlap edge");
+                dev::ContigArgs a2{x, static_cast<char*>(out_) + f0 * plane * out_elem, smap_, ny_, nc_, fc, shift_,
+                                   shift_, scale, plan_.tw_x.as<float2>()};
+                ck(dev::launch_contig(nx_, +1, mode_, a2, full ? ovl_s2_ : ovl_tail_s2_, side_),
+                   name() + "/axis0+combine");
+            }
+            // join
+            ck(cudaEventRecord(ev[k + 1], side_), "overlap join");
+            ck(cudaStreamWaitEvent(s, ev[k + 1], 0), "overlap join");
+            mark(s);
+            return;
+        }
         for (std::uint64_t f0 = 0; f0 < nf_; f0 += chunk_) {
             const std::uint64_t fc = std::min(chunk_, nf_ - f0);
             const bool full = fc == chunk_;
@@ -872,6 +930,22 @@ private:
     dev::LaunchShape tail_s1_, tail_s2_;
     bool tma_ = false;
     dev::LaunchShape tail_tma_;
+    bool overlap_ = false;
+    std::uint64_t ovl_chunk_ = 8;
+    dev::LaunchShape ovl_s1_, ovl_s2_, ovl_tail_s1_, ovl_tail_s2_;
+    cudaStream_t side_ = nullptr;
+    std::vector<cudaEvent_t> ovl_events_;
+
+public:
+    ~ReconProcess() override {
+        if (side_) {
+            cudaStreamSynchronize(side_);
+            cudaStreamDestroy(side_);
+        }
+        for (cudaEvent_t e : ovl_events_) cudaEventDestroy(e);
+    }
+
+private:
     bool cluster_ = false;
     dev::ClusterPlan cplan_;
     dev::ClusterMap cmap_{};

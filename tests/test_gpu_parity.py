@@ -640,3 +640,18 @@ def test_staged_map_combine(s, monkeypatch, nx, ny, nc, nf, shift):
     if shift:
         ref = np.fft.fftshift(ref, axes=ax)
     assert relmax(M, ref) <= TOL
+
+
+@pytest.mark.parametrize("method", ["sens_recon", "rss_recon"])
+def test_recon_overlap_pipeline_bitexact(s, method):
+    """"overlap": true -- chunked axis-1/combine graph branches (fork/join over a
+    side stream in the captured graph) give the same bits as the serial chain."""
+    nx, nc, nf = 256, 3, 21
+    rng = np.random.default_rng(21)
+    Y = cplx(rng, nx, nx, nc, nf)
+    S = cplx(rng, nx, nx, nc)
+    ins = [Y, S] if method == "sens_recon" else [Y]
+    dt = np.complex64 if method == "sens_recon" else np.float32
+    (A,), p = run_process(s, method, ins, [((nx, nx, nf), dt)], {"overlap": True})
+    (B,), _ = run_process(s, method, ins, [((nx, nx, nf), dt)], {"overlap": False})
+    assert beq(A, B)
