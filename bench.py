@@ -198,6 +198,8 @@ def run_ours(args):
     from paper_1807_11830_b200 import hetreco as h
 
     rank, world, local = dist_setup(args.gpus)
+    # host placement: this rank's thread and pinned buffers on its GPU's NUMA node
+    numa_node = h.bind_to_device_numa(local)
     devs = h.enumerate_devices()
     s = h.ComputeSession(device=devs[local])
     Y, S = make_inputs(1234 + rank)
@@ -308,7 +310,8 @@ def run_ours(args):
                 "warmup": args.warmup, "ms_per_step": t_max / args.steps * 1e3, "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": "f32 (complex64 I/O, fp32 FFT and coil accumulation)",
                 "data": "synthetic (seeded N(0,1) k-space, normalised random sensitivity maps)",
-                "config": dict(CONFIG, parallelism=f"frame-slab x{world} (no collective)"),
+                "config": dict(CONFIG, parallelism=f"frame-slab x{world} (no collective)",
+                               host_numa_node_rank0=numa_node),
                 "impl": "hetreco-b200",
                 "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu, "clocks": clocks,
                 "gpu_launches": 2 * args.steps, "other_configs": extras}

@@ -274,6 +274,13 @@ int hetreco_nvrtc_compile_check(const char* unit_name, const char* source, char*
                                 char* log, uint64_t log_cap);
 int hetreco_nvrtc_available(int* available);
 
+/* ---- NUMA placement for multi-GPU streaming (SURVEY.md §8 e) ------------------
+ * Each rank binds its host thread to the NUMA node of its GPU before
+ * allocating the pinned slab it streams from (first-touch placement). */
+int hetreco_device_numa_node(int ordinal, int* node);       /* -1: no NUMA info */
+int hetreco_bind_numa_node(int node, int* cpus);            /* node < 0: no-op */
+int hetreco_parse_cpulist(const char* text, int* cpus, int cap, int* count);
+
 #if defined(__GNUC__)
 #pragma GCC visibility pop
 #endif

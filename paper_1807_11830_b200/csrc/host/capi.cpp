@@ -11,6 +11,7 @@
 
 #include "../kernels/launch.hpp"
 #include "hetreco_b200/io.hpp"
+#include "hetreco_b200/numa.hpp"
 #include "hetreco_b200/phantom.hpp"
 #include "nvrtc_compiler.hpp"
 #include "hetreco_b200/processes.hpp"
@@ -849,5 +850,31 @@ extern "C" int hetreco_nvrtc_available(int* available) {
     return guard([&] {
         need(available, "available");
         *available = nvrtc::available() ? 1 : 0;
+    });
+}
+
+// ---- NUMA placement (SURVEY.md §8 e) ---------------------------------------------------
+
+extern "C" int hetreco_device_numa_node(int ordinal, int* node) {
+    return guard([&] {
+        need(node, "node");
+        *node = device_numa_node(ordinal);
+    });
+}
+
+extern "C" int hetreco_bind_numa_node(int node, int* cpus) {
+    return guard([&] {
+        const int n = bind_thread_to_numa_node(node);
+        if (cpus) *cpus = n;
+    });
+}
+
+extern "C" int hetreco_parse_cpulist(const char* text, int* cpus, int cap, int* count) {
+    return guard([&] {
+        need(text, "text");
+        need(count, "count");
+        const std::vector<int> v = parse_cpulist(text);
+        *count = int(v.size());
+        for (int i = 0; i < int(v.size()) && i < cap && cpus; ++i) cpus[i] = v[std::size_t(i)];
     });
 }

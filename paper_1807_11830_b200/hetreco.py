@@ -89,6 +89,7 @@ EXPORTED = [
     "hetreco_mat_variable", "hetreco_mat_free", "hetreco_mat_write", "hetreco_image_write", "hetreco_raw_write",
     "hetreco_gen_phantom", "hetreco_phantom_blobs", "hetreco_nvrtc_compile_check", "hetreco_nvrtc_available",
     "hetreco_cuda_supports_source", "hetreco_cuda_compile", "hetreco_cuda_execute_unit",
+    "hetreco_device_numa_node", "hetreco_bind_numa_node", "hetreco_parse_cpulist",
 ]
 
 
@@ -153,6 +154,8 @@ def lib():
         "hetreco_nvrtc_compile_check": ([pc, pc, vp, u64, vp, u64], i32), "hetreco_nvrtc_available": ([vp], i32),
         "hetreco_cuda_supports_source": ([vp, vp], i32), "hetreco_cuda_compile": ([vp, i32, vp, vp, vp, u64], i32),
         "hetreco_cuda_execute_unit": ([vp, pc, pc, u64, u64, u64, u64, vp, u64, u64], i32),
+        "hetreco_device_numa_node": ([i32, vp], i32), "hetreco_bind_numa_node": ([i32, vp], i32),
+        "hetreco_parse_cpulist": ([pc, vp, i32, vp], i32),
     })
     lenient = os.environ.get("HETRECO_LIB_LENIENT") == "1"  # A/B runs against older builds
     for name, (args, res) in sig.items():
@@ -889,3 +892,35 @@ def compile_check(unit_name: str, source: str):
         msg = lib().hetreco_last_error().decode(errors="replace")
         raise ERRORS.get(rc, HetrecoError)(msg)
     return [n for n in names.value.decode().split("\n") if n], log.value.decode(errors="replace")
+
+
+# ---------------------------------------------------------------------------
+# NUMA placement (multi-GPU streaming, SURVEY.md §8 e)
+# ---------------------------------------------------------------------------
+
+
+def device_numa_node(ordinal: int) -> int:
+    n = C.c_int()
+    _ck(lib().hetreco_device_numa_node(ordinal, C.byref(n)))
+    return n.value
+
+
+def bind_numa_node(node: int) -> int:
+    """Restricts the calling thread (and later threads) to the CPUs of `node`."""
+    n = C.c_int()
+    _ck(lib().hetreco_bind_numa_node(node, C.byref(n)))
+    return n.value
+
+
+def bind_to_device_numa(ordinal: int) -> int:
+    """Binds the calling thread to its GPU's NUMA node; returns the node (-1: none)."""
+    node = device_numa_node(ordinal)
+    bind_numa_node(node)
+    return node
+
+
+def parse_cpulist(text: str) -> list:
+    buf = (C.c_int * 4096)()
+    n = C.c_int()
+    _ck(lib().hetreco_parse_cpulist(text.encode(), buf, 4096, C.byref(n)))
+    return list(buf[: min(n.value, 4096)])

@@ -55,3 +55,26 @@ def test_gloo_world2_max_over_ranks():
         assert p.exitcode == 0
     assert [(b, e) for _, b, e, _ in res] == [(0, 15), (15, 30)]
     assert all(t == 1.0 for *_, t in res)
+
+
+def test_numa_cpulist_and_bind():
+    """Host placement helpers used by each rank before it allocates its pinned
+    slab (SURVEY.md §8 e)."""
+    import os
+
+    from paper_1807_11830_b200 import hetreco as h
+    assert h.parse_cpulist("0-3,8,10-11\n") == [0, 1, 2, 3, 8, 10, 11]
+    assert h.parse_cpulist("5") == [5]
+    with pytest.raises(h.InvalidArgument):
+        h.parse_cpulist("3-1")
+    with pytest.raises(h.InvalidArgument):
+        h.parse_cpulist("a-b")
+    assert h.bind_numa_node(-1) == 0  # no NUMA information: no-op
+    before = os.sched_getaffinity(0)
+    try:
+        if os.path.exists("/sys/devices/system/node/node0/cpulist"):
+            n = h.bind_numa_node(0)
+            node0 = set(h.parse_cpulist(open("/sys/devices/system/node/node0/cpulist").read()))
+            assert n == len(node0) and os.sched_getaffinity(0) <= node0
+    finally:
+        os.sched_setaffinity(0, before)
