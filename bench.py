@@ -199,6 +199,8 @@ def run_ours(args):
 
     rank, world, local = dist_setup(args.gpus)
     # host placement: this rank's thread and pinned buffers on its GPU's NUMA node
+    # (the CPU-baseline leg below gets the whole host back)
+    all_cpus = os.sched_getaffinity(0)
     numa_node = h.bind_to_device_numa(local)
     devs = h.enumerate_devices()
     s = h.ComputeSession(device=devs[local])
@@ -299,6 +301,7 @@ def run_ours(args):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        os.sched_setaffinity(0, all_cpus)
         cpu = cpu_baseline(Y, S)
 
     extras = None
