@@ -49,6 +49,8 @@ public:
     std::string get_string(std::string_view key, std::string_view fallback) const;
     void require_known(std::initializer_list<std::string_view> known) const;
     std::size_t size() const { return values_.size(); }
+    // copy without `key` (generic keys consumed by Process::init)
+    ProcessParams without(std::string_view key) const;
 
 private:
     const Value* find(std::string_view key) const;
@@ -114,6 +116,7 @@ private:
     mutable LaunchStats stats_;
     struct Timing;
     std::unique_ptr<Timing> timing_;
+    int timing_mode_ = 0;  // "launch_timing": 0 every, 1 sampled, 2 off
 };
 
 // A process whose device work is recorded once into a CUDA graph.

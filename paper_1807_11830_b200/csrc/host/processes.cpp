@@ -164,6 +164,12 @@ std::string ProcessParams::get_string(std::string_view k, std::string_view fb) c
     throw InvalidParams("parameter '" + std::string(k) + "' is not a string");
 }
 
+ProcessParams ProcessParams::without(std::string_view key) const {
+    ProcessParams p = *this;
+    if (auto it = p.values_.find(key); it != p.values_.end()) p.values_.erase(it);
+    return p;
+}
+
 void ProcessParams::require_known(std::initializer_list<std::string_view> known) const {
     for (const auto& [k, v] : values_) {
         bool ok = false;
@@ -179,12 +185,26 @@ void ProcessParams::require_known(std::initializer_list<std::string_view> known)
 
 // ---- Process ----------------------------------------------------------------------------
 
+// Device-side launch timing (LaunchStats, process.hpp:55-64).  A launch that
+// is queued behind the previous one on the same stream starts exactly when
+// that one stops, so back-to-back launches record only a stop event and chain
+// to the previous stop (one cudaEventRecord per launch instead of two: the
+// event records were 3/4 of the host cost of a tiny process launch); a launch
+// onto an idle stream records its own start.
 struct Process::Timing {
     static constexpr int kRing = 128;
     int device = -1;
     cudaStream_t stream = nullptr;
     cudaEvent_t start[kRing]{}, stop[kRing]{};
+    bool chained[kRing]{};
     int head = 0, pending = 0;
+    int last = -1;  // slot of the most recent launch (its stop event stays valid until resolved + reused)
+    // "launch_timing": 0 = every launch (default), 1 = every kSample-th launch
+    // (totals extrapolated from the sampled mean), 2 = off
+    int mode = 0;
+    static constexpr std::uint64_t kSample = 16;
+    double sampled_seconds = 0.0;
+    std::uint64_t sampled = 0;
 };
 
 Process::Process(ComputeSession& s, std::string name) : session_(s), name_(std::move(name)) {}
@@ -224,7 +244,13 @@ DataHandle Process::require_output() const {
 void Process::init(const ProcessParams& params) {
     if (state_ != ProcessState::Created) throw AlreadyInitialized("process '" + name_ + "' is already initialized");
     const auto t0 = std::chrono::steady_clock::now();
-    on_init(params);
+    // generic key: "launch_timing" = "every" | "sampled" | "off" (LaunchStats cost:
+    // a timed CUDA event record is ~3 us of host time per launch on B200)
+    const std::string lt = params.get_string("launch_timing", "every");
+    if (lt != "every" && lt != "sampled" && lt != "off")
+        throw InvalidParams("launch_timing must be \"every\", \"sampled\" or \"off\"");
+    timing_mode_ = lt == "every" ? 0 : lt == "sampled" ? 1 : 2;
+    on_init(params.without("launch_timing"));
     state_ = ProcessState::Initialized;
     rebound_ = false;
     stats_.init_calls += 1;
@@ -249,12 +275,27 @@ void Process::launch() {
         }
     }
     Timing& t = *timing_;
+    t.mode = timing_mode_;
+    if (t.mode == 2 || (t.mode == 1 && stats_.launches % Timing::kSample != 0)) {
+        on_launch();
+        stats_.launches += 1;
+        if (t.mode == 1 && t.sampled) stats_.total_launch_seconds = t.sampled_seconds / double(t.sampled) * double(stats_.launches);
+        t.last = -1;  // an untimed launch breaks the chain
+        return;
+    }
     if (t.pending == Timing::kRing) resolve_timings();
     const int slot = (t.head + t.pending) % Timing::kRing;
     cudaSetDevice(t.device);
-    cudaEventRecord(t.start[slot], t.stream);
+    // chain to the previous launch only while it is still queued/running
+    const bool chain = t.pending > 0 && t.last >= 0 && cudaEventQuery(t.stop[t.last]) == cudaErrorNotReady;
+    if (!chain) {
+        cudaGetLastError();  // a completed query is not an error
+        cudaEventRecord(t.start[slot], t.stream);
+    }
+    t.chained[slot] = chain;
     on_launch();
     cudaEventRecord(t.stop[slot], t.stream);
+    t.last = slot;
     t.pending += 1;
     stats_.launches += 1;
 }
@@ -271,9 +312,16 @@ void Process::resolve_timings() const {
             t.pending = 0;
             throw DeviceError(name_, cudaGetErrorString(e));
         }
-        cudaEventElapsedTime(&ms, t.start[s], t.stop[s]);
+        const cudaEvent_t from = t.chained[s] ? t.stop[(s + Timing::kRing - 1) % Timing::kRing] : t.start[s];
+        cudaEventElapsedTime(&ms, from, t.stop[s]);
         stats_.last_launch_seconds = double(ms) * 1e-3;
-        stats_.total_launch_seconds += stats_.last_launch_seconds;
+        if (t.mode == 1) {
+            t.sampled_seconds += stats_.last_launch_seconds;
+            t.sampled += 1;
+            stats_.total_launch_seconds = t.sampled_seconds / double(t.sampled) * double(stats_.launches);
+        } else {
+            stats_.total_launch_seconds += stats_.last_launch_seconds;
+        }
         t.head = (t.head + 1) % Timing::kRing;
         t.pending -= 1;
     }

@@ -655,3 +655,25 @@ def test_recon_overlap_pipeline_bitexact(s, method):
     (A,), p = run_process(s, method, ins, [((nx, nx, nf), dt)], {"overlap": True})
     (B,), _ = run_process(s, method, ins, [((nx, nx, nf), dt)], {"overlap": False})
     assert beq(A, B)
+
+
+def test_launch_timing_modes(s):
+    """LaunchStats under "launch_timing": every launch timed (default), every
+    16th (totals extrapolated), or off; bad values rejected."""
+    x = np.asfortranarray(np.random.default_rng(3).random((256, 256), dtype=np.float32))
+    hx = s.register_data([x])
+    hy = s.allocate_data([((256, 256), np.float32)])
+    for mode in ("every", "sampled", "off"):
+        p = h.Process(s, "negate").set_input(hx).set_output(hy).init({"max_value": 1.0, "launch_timing": mode})
+        for _ in range(40):
+            p.launch()
+        st = p.stats()
+        assert st.launches == 40 and st.init_calls == 1
+        if mode == "off":
+            assert st.total_launch_seconds == 0.0
+        else:
+            assert st.total_launch_seconds > 0 and st.last_launch_seconds > 0
+            assert abs(st.mean_launch_seconds() * 40 - st.total_launch_seconds) < 1e-9
+        assert beq(s.fetch_data(hy).arrays[0], o.negate(x, 1.0))
+    with pytest.raises(h.InvalidParams):
+        h.Process(s, "negate").set_input(hx).set_output(hy).init({"launch_timing": "sometimes"})
