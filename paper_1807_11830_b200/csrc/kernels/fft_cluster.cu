@@ -127,7 +127,6 @@ struct ClusterArgs {
     std::uint32_t coils, frames;
     int shift;
     float scale;
-    int diag_local;  // diagnostics only: transpose into the own CTA (wrong result, no DSMEM traffic)
 };
 
 template <int MODE, int kCL>
@@ -275,8 +274,7 @@ __global__ void __launch_bounds__(Geo<kCL>::threads, Geo<kCL>::min_blocks)
             constexpr int y0 = T * ms.value;  // y' = jA + y0, jA < T <= kRY
             constexpr int q = y0 / kRY;       // destination CTA (compile time)
             const int y = jA + y0;
-            const std::uint32_t qq = a.diag_local ? r : std::uint32_t(q);
-            st_async(mapa(dst + std::uint32_t((y % kRY) * kLS) * 8, qq), v[m.value], mapa(rb, qq));
+            st_async(mapa(dst + std::uint32_t((y % kRY) * kLS) * 8, q), v[m.value], mapa(rb, q));
         });
     };
 
@@ -456,7 +454,7 @@ cudaError_t launch_cluster(Combine mode, const ClusterMap& m, const ClusterLaunc
                            cudaStream_t st) {
     if (p.clusters <= 0) return cudaErrorInvalidConfiguration;
     ClusterArgs ka{a.smap, a.out, a.ws, a.cnt, a.tw, std::uint32_t(a.coils), std::uint32_t(a.frames), a.shift,
-                   a.scale, std::getenv("HETRECO_CLUSTER_DIAG_LOCAL") ? 1 : 0};
+                   a.scale};
     const CUtensorMap& map = *reinterpret_cast<const CUtensorMap*>(m.bytes);
     const bool sense = mode == Combine::Sense;
     if (p.cl == 16)
