@@ -104,6 +104,35 @@ int cp_occ(int smem) {
     return blocks_per_sm(k_fft_combine_cp<N, MODE, G>, G * LineFFT<N>::T, smem);
 }
 
+template <int n>
+LaunchShape plan_cp_n(Combine mode, std::uint64_t items, int sms) {
+    LaunchShape s;
+    if constexpr (n >= 16) {
+        constexpr int G = cp_groups<n>();
+        s.rq = LineFFT<n>::R;
+        s.block = G * LineFFT<n>::T;
+        s.smem = G * line_stride<n>() * 8;
+        const int occ = mode == Combine::Sense ? cp_occ<n, 1>(s.smem) : cp_occ<n, 2>(s.smem);
+        s.grid = int(std::min<std::uint64_t>(items, std::uint64_t(sms) * occ));
+        s.variant = 128;
+    }
+    return s;
+}
+
+template <int n>
+cudaError_t launch_cp_n(Combine mode, const ContigArgs& a, const LaunchShape& s, std::uint32_t items, cudaStream_t st) {
+    if constexpr (n >= 16) {
+        constexpr int G = cp_groups<n>();
+        if (mode == Combine::Sense)
+            k_fft_combine_cp<n, 1, G><<<s.grid, s.block, s.smem, st>>>(a, items);
+        else
+            k_fft_combine_cp<n, 2, G><<<s.grid, s.block, s.smem, st>>>(a, items);
+        return cudaGetLastError();
+    } else {
+        return cudaErrorInvalidValue;
+    }
+}
+
 }  // namespace
 
 bool combine_cp_preferred(std::uint64_t N, std::uint64_t items, std::uint64_t coils, int sms) {
@@ -120,18 +149,8 @@ LaunchShape plan_combine_cp(std::uint64_t N, Combine mode, std::uint64_t items, 
     LaunchShape s;
     if (!fft_size_supported(N) || N < 16 || mode == Combine::None) return s;
     switch (N) {
-#define X(n)                                                                                          \
-    case n:                                                                                           \
-        if constexpr (n >= 16) {                                                                      \
-            constexpr int G = cp_groups<n>();                                                         \
-            s.rq = LineFFT<n>::R;                                                                     \
-            s.block = G * LineFFT<n>::T;                                                              \
-            s.smem = G * line_stride<n>() * 8;                                                        \
-            const int occ = mode == Combine::Sense ? cp_occ<n, 1>(s.smem) : cp_occ<n, 2>(s.smem);     \
-            s.grid = int(std::min<std::uint64_t>(items, std::uint64_t(sms) * occ));                   \
-            s.variant = 128;                                                                          \
-        }                                                                                             \
-        break;
+#define X(n) \
+    case n: s = plan_cp_n<n>(mode, items, sms); break;
         HETRECO_FFT_SIZES(X)
 #undef X
     }
@@ -146,17 +165,8 @@ cudaError_t launch_combine_cp(std::uint64_t N, Combine mode, const ContigArgs& a
     if (items64 >= (std::uint64_t(1) << 32)) return cudaErrorInvalidValue;
     const std::uint32_t items = std::uint32_t(items64);
     switch (N) {
-#define X(n)                                                                                        \
-    case n:                                                                                         \
-        if constexpr (n >= 16) {                                                                    \
-            constexpr int G = cp_groups<n>();                                                       \
-            if (mode == Combine::Sense)                                                             \
-                k_fft_combine_cp<n, 1, G><<<s.grid, s.block, s.smem, st>>>(a, items);               \
-            else                                                                                    \
-                k_fft_combine_cp<n, 2, G><<<s.grid, s.block, s.smem, st>>>(a, items);               \
-            return cudaGetLastError();                                                              \
-        }                                                                                           \
-        break;
+#define X(n) \
+    case n: return launch_cp_n<n>(mode, a, s, items, st);
         HETRECO_FFT_SIZES(X)
 #undef X
     }

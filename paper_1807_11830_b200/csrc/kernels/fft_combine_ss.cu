@@ -100,6 +100,32 @@ constexpr int ss_smem() {
     return (kSsLines * line_stride<N>() + 2 * N) * 8;
 }
 
+template <int n>
+LaunchShape plan_ss_n(std::uint64_t ny, std::uint64_t frames, int sms) {
+    LaunchShape s;
+    if constexpr (n >= 64) {
+        s.rq = LineFFT<n>::R;
+        s.block = kSsLines * LineFFT<n>::T;
+        s.smem = ss_smem<n>();
+        const std::uint64_t groups = ny * ((frames + kSsLines - 1) / kSsLines);
+        const int occ = blocks_per_sm(k_fft_combine_ss<n, kSsLines>, s.block, s.smem);
+        s.grid = int(std::min<std::uint64_t>(groups, std::uint64_t(sms) * occ));
+        s.variant = 256;
+    }
+    return s;
+}
+
+template <int n>
+cudaError_t launch_ss_n(const ContigArgs& a, const LaunchShape& s, std::uint32_t gpy, std::uint32_t groups,
+                        cudaStream_t st) {
+    if constexpr (n >= 64) {
+        k_fft_combine_ss<n, kSsLines><<<s.grid, s.block, s.smem, st>>>(a, gpy, groups);
+        return cudaGetLastError();
+    } else {
+        return cudaErrorInvalidValue;
+    }
+}
+
 }  // namespace
 
 bool combine_ss_supported(std::uint64_t N) {
@@ -115,18 +141,8 @@ bool combine_ss_supported(std::uint64_t N) {
 LaunchShape plan_combine_ss(std::uint64_t N, std::uint64_t ny, std::uint64_t frames, int sms) {
     LaunchShape s;
     switch (N) {
-#define X(n)                                                                                        \
-    case n:                                                                                         \
-        if constexpr (n >= 64) {                                                                    \
-            s.rq = LineFFT<n>::R;                                                                   \
-            s.block = kSsLines * LineFFT<n>::T;                                                     \
-            s.smem = ss_smem<n>();                                                                  \
-            const std::uint64_t groups = ny * ((frames + kSsLines - 1) / kSsLines);                 \
-            const int occ = blocks_per_sm(k_fft_combine_ss<n, kSsLines>, s.block, s.smem);          \
-            s.grid = int(std::min<std::uint64_t>(groups, std::uint64_t(sms) * occ));                \
-            s.variant = 256;                                                                        \
-        }                                                                                           \
-        break;
+#define X(n) \
+    case n: s = plan_ss_n<n>(ny, frames, sms); break;
         HETRECO_FFT_SIZES(X)
 #undef X
     }
@@ -140,14 +156,8 @@ cudaError_t launch_combine_ss(std::uint64_t N, const ContigArgs& a, const Launch
     const std::uint64_t groups = a.ny * gpy;
     if (groups >= (std::uint64_t(1) << 32)) return cudaErrorInvalidValue;
     switch (N) {
-#define X(n)                                                                                                 \
-    case n:                                                                                                  \
-        if constexpr (n >= 64) {                                                                             \
-            k_fft_combine_ss<n, kSsLines><<<s.grid, s.block, s.smem, st>>>(a, std::uint32_t(gpy),            \
-                                                                            std::uint32_t(groups));          \
-            return cudaGetLastError();                                                                       \
-        }                                                                                                    \
-        break;
+#define X(n) \
+    case n: return launch_ss_n<n>(a, s, std::uint32_t(gpy), std::uint32_t(groups), st);
         HETRECO_FFT_SIZES(X)
 #undef X
     }
