@@ -11,6 +11,8 @@
 // semantics as k_fft_combine's fp32 variant (complex_element_prod.cl.src:9-19,
 // ximage_sum.cl.src:6-23, rss_combine.cl.src:5-20), different fp32 summation
 // order (within the 1e-5 tolerance).
+#include <cstdlib>
+
 #include "fft_kernels.cuh"
 
 namespace hetreco::dev {
@@ -137,12 +139,16 @@ cudaError_t launch_cp_n(Combine mode, const ContigArgs& a, const LaunchShape& s,
 
 bool combine_cp_preferred(std::uint64_t N, std::uint64_t items, std::uint64_t coils, int sms) {
     if (!fft_size_supported(N) || N < 16 || coils < 2) return false;
+    if (const char* e = std::getenv("HETRECO_COMBINE_CP"); e && *e) return *e == '1';  // force on / off
     const int R = points_for(N, 0);
     const std::uint64_t T = N / std::uint64_t(R);
-    // the coil-serial kernel would have under ~2 warps of lines per SM
-    // (measured: C2/C4, 0.9 warps/SM -> coil-parallel 22 % faster; a 512^2 x
-    // 2-frame streaming chunk, 7 warps/SM -> coil-serial 18 % faster)
-    return items * T < std::uint64_t(sms) * 64;
+    // warps of lines per SM the coil-serial kernel would have.  Measured:
+    // C2/C4 (0.9 warps/SM) coil-parallel 22 % faster; 512^2 x 2-frame chunk
+    // (7 warps/SM, T = 32) coil-serial 18 % faster; 256^2 C3 (26 warps/SM)
+    // coil-serial 5 % faster; 160^2 C3 (8 warps/SM, T = 8 threads per line)
+    // coil-parallel 12 % faster (SENSE), 19 % (RSS).
+    const std::uint64_t warps = items * T / 32 / std::uint64_t(sms);
+    return warps < 2 || (T < 16 && warps < 16);
 }
 
 LaunchShape plan_combine_cp(std::uint64_t N, Combine mode, std::uint64_t items, int sms) {
