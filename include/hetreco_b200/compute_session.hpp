@@ -47,6 +47,13 @@ public:
 
     // ---- data (session.hpp:73-90) ----
     DataHandle register_data(const Data& data);
+    // register_data from borrowed host buffers (no intermediate NDArray copy;
+    // the C-ABI path): one logical transfer, same packing and counters.
+    struct HostArrayRef {
+        ArrayShape shape;
+        const void* data = nullptr;
+    };
+    DataHandle register_host(std::span<const HostArrayRef> arrays, DataKind kind = DataKind::Generic);
     Data fetch_data(DataHandle handle, HostMemory memory = HostMemory::Pageable);
     void release_data(DataHandle handle);
     const LayoutDescriptor& layout_of(DataHandle handle) const;
@@ -85,7 +92,7 @@ private:
         DataKind kind = DataKind::Generic;
     };
     const Entry& resolve(DataHandle handle) const;
-    DataHandle insert(const LayoutDescriptor& layout, DataKind kind, const Data* payload);
+    DataHandle insert(const LayoutDescriptor& layout, DataKind kind, const std::vector<const void*>* payload);
 
     Backend& backend_;
     DeviceDescriptor device_;

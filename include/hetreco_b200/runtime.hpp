@@ -33,6 +33,10 @@ typedef struct CUlib_st* cudaLibrary_t;
 
 namespace hetreco {
 
+namespace detail {
+class HostStager;  // pinned-ring staging of pageable transfers (csrc/host/host_stager.hpp)
+}
+
 // ---- devices (device.hpp:15-114) ---------------------------------------------------
 
 enum class DeviceType { Cpu, Gpu, Accelerator };
@@ -223,6 +227,9 @@ private:
     std::byte* ring_dev_ = nullptr;
     std::uint64_t ring_size_ = 0, ring_head_ = 0;
     mutable std::string last_kernel_;
+    // pageable host <-> device transfers through a pinned ring (lazily built)
+    mutable std::unique_ptr<detail::HostStager> stager_;
+    detail::HostStager& stager() const;
     // run-time compiled (NVRTC) kernels: "<unit tag>/<name>" -> entry point
     std::unordered_map<std::string, cudaKernel_t> jit_;
     std::vector<cudaLibrary_t> jit_libs_;

@@ -361,15 +361,11 @@ int hetreco_register_data(hetreco_session s, int kind, int count, const hetreco_
                           hetreco_handle* out) {
     return guard([&] {
         need(out, "out");
-        Data d;
-        d.kind = kind_of(kind);
-        for (int i = 0; i < count; ++i) {
-            const ArrayShape sh = shape_of(arrays[i]);
-            NDArray a(sh.element_type, sh.dims);
-            if (arrays[i].host) std::memcpy(a.bytes().data(), arrays[i].host, a.byte_size());
-            d.arrays.push_back(std::move(a));
-        }
-        *out = C(S(s).register_data(d));
+        if (count < 0) throw InvalidArgument("count must be >= 0");
+        // borrowed host buffers straight to the device (no intermediate copy)
+        std::vector<ComputeSession::HostArrayRef> refs;
+        for (int i = 0; i < count; ++i) refs.push_back({shape_of(arrays[i]), arrays[i].host});
+        *out = C(S(s).register_host(refs, kind_of(kind)));
     });
 }
 

@@ -10,6 +10,7 @@
 #include "../kernels/launch.hpp"
 #include "hetreco_b200/runtime.hpp"
 
+#include "host_stager.hpp"
 #include "nvrtc_compiler.hpp"
 
 namespace hetreco {
@@ -65,6 +66,13 @@ CudaBackend::CudaBackend(int ordinal, std::uint64_t capacity) : ordinal_(ordinal
     desc_.base_alignment_bytes = 256;
     desc_.supports_source_kernels = nvrtc::available();
     make_current();
+    cudaMemPool_t pool = nullptr;
+    if (cudaDeviceGetDefaultMemPool(&pool, ordinal) == cudaSuccess) {
+        std::uint64_t keep = ~std::uint64_t(0);
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    } else {
+        cudaGetLastError();
+    }
     ck(cudaStreamCreateWithFlags(&compute_, cudaStreamNonBlocking), "cudaStreamCreate");
     ck(cudaStreamCreateWithFlags(&h2d_, cudaStreamNonBlocking), "cudaStreamCreate");
     ck(cudaStreamCreateWithFlags(&d2h_, cudaStreamNonBlocking), "cudaStreamCreate");
@@ -78,7 +86,10 @@ CudaBackend::CudaBackend(int ordinal, std::uint64_t capacity) : ordinal_(ordinal
 CudaBackend::~CudaBackend() {
     cudaSetDevice(ordinal_);
     cudaStreamSynchronize(compute_);
-    for (auto& [id, b] : bufs_) cudaFree(b.ptr);
+    for (auto& [id, b] : bufs_) cudaFreeAsync(b.ptr, compute_);
+    cudaStreamSynchronize(compute_);
+    cudaMemPool_t pool = nullptr;
+    if (cudaDeviceGetDefaultMemPool(&pool, ordinal_) == cudaSuccess) cudaMemPoolTrimTo(pool, 0);
     cudaFree(ring_dev_);
     cudaFreeHost(ring_host_);
     cudaEventDestroy(ev_compute_);
@@ -87,6 +98,7 @@ CudaBackend::~CudaBackend() {
     cudaStreamDestroy(h2d_);
     cudaStreamDestroy(d2h_);
     for (cudaLibrary_t l : jit_libs_) cudaLibraryUnload(l);
+    stager_.reset();
 }
 
 void CudaBackend::make_current() const { ck(cudaSetDevice(ordinal_), "cudaSetDevice"); }
@@ -104,11 +116,15 @@ BufferId CudaBackend::allocate(std::uint64_t bytes) {
                                 std::to_string(capacity_ - used_) + " of " + std::to_string(capacity_) +
                                 " bytes free)");
     make_current();
+    // stream-ordered allocation from the device pool (kept warm: the release
+    // threshold is unlimited), so register/release cycles do not pay a
+    // cudaMalloc/cudaFree (and its device-wide sync) each time
     void* p = nullptr;
-    const cudaError_t e = cudaMalloc(&p, bytes ? bytes : 1);
+    const cudaError_t e = cudaMallocAsync(&p, bytes ? bytes : 1, compute_);
     if (e != cudaSuccess) {
         cudaGetLastError();
-        throw AllocationFailure("cudaMalloc of " + std::to_string(bytes) + " bytes failed: " + cudaGetErrorString(e));
+        throw AllocationFailure("cudaMallocAsync of " + std::to_string(bytes) + " bytes failed: " +
+                                cudaGetErrorString(e));
     }
     // zero-filled like the reference's buffers (backend.cpp:137-141), in queue order
     ck(cudaMemsetAsync(p, 0, bytes ? bytes : 1, compute_), "cudaMemsetAsync");
@@ -123,10 +139,20 @@ void CudaBackend::release(BufferId id) {
     auto it = bufs_.find(id);
     if (it == bufs_.end()) throw UnknownHandle("release of unknown buffer " + std::to_string(id));
     make_current();
-    cudaStreamSynchronize(compute_);  // in-flight kernels may still read it
-    cudaFree(it->second.ptr);
+    // stream-ordered: in-flight work on the compute stream finishes first
+    cudaFreeAsync(it->second.ptr, compute_);
     used_ -= it->second.size;
     bufs_.erase(it);
+}
+
+// Transfers of at least this many bytes from/to pageable memory go through
+// the pinned staging ring (host_stager.hpp); smaller ones and page-locked
+// buffers use a direct cudaMemcpyAsync.
+constexpr std::size_t kStageMin = std::size_t(4) << 20;
+
+detail::HostStager& CudaBackend::stager() const {
+    if (!stager_) stager_ = std::make_unique<detail::HostStager>(ordinal_);
+    return *stager_;
 }
 
 void CudaBackend::upload(BufferId id, std::uint64_t off, std::span<const std::byte> bytes) {
@@ -135,6 +161,14 @@ void CudaBackend::upload(BufferId id, std::uint64_t off, std::span<const std::by
     check_window("upload", off, bytes.size(), b.size);
     if (bytes.empty()) return;
     make_current();
+    if (bytes.size() >= kStageMin && !detail::HostStager::is_pinned(bytes.data())) {
+        try {
+            stager().upload(static_cast<char*>(b.ptr) + off, bytes.data(), bytes.size(), compute_);
+        } catch (const DeviceError& e) {
+            throw DeviceError(last_kernel_.empty() ? "<upload>" : last_kernel_, e.what());
+        }
+        return;
+    }
     ck(cudaMemcpyAsync(static_cast<char*>(b.ptr) + off, bytes.data(), bytes.size(), cudaMemcpyHostToDevice,
                        compute_),
        "cudaMemcpyAsync(H2D)");
@@ -148,6 +182,14 @@ void CudaBackend::download(BufferId id, std::uint64_t off, std::span<std::byte> 
     check_window("download", off, into.size(), b.size);
     if (into.empty()) return;
     make_current();
+    if (into.size() >= kStageMin && !detail::HostStager::is_pinned(into.data())) {
+        try {
+            stager().download(into.data(), static_cast<const char*>(b.ptr) + off, into.size(), compute_);
+        } catch (const DeviceError& e) {
+            throw DeviceError(last_kernel_.empty() ? "<download>" : last_kernel_, e.what());
+        }
+        return;
+    }
     ck(cudaMemcpyAsync(into.data(), static_cast<const char*>(b.ptr) + off, into.size(), cudaMemcpyDeviceToHost,
                        compute_),
        "cudaMemcpyAsync(D2H)");

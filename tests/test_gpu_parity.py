@@ -677,3 +677,26 @@ def test_launch_timing_modes(s):
         assert beq(s.fetch_data(hy).arrays[0], o.negate(x, 1.0))
     with pytest.raises(h.InvalidParams):
         h.Process(s, "negate").set_input(hx).set_output(hy).init({"launch_timing": "sometimes"})
+
+
+def test_large_pageable_transfers_through_staging_ring(s):
+    """register_data / fetch_data of pageable arrays >= 4 MiB go through the
+    pinned staging ring (host_stager.cpp): multi-array packing, sizes that
+    are not multiples of the 16 MiB slot, and page-locked buffers (direct)."""
+    rng = np.random.default_rng(11)
+    a = rng.integers(0, 255, 5 * 2**20 + 13, dtype=np.uint8)
+    b = np.asfortranarray(rng.standard_normal((1031, 977, 5)).astype(np.complex64))   # ~38 MiB
+    c = rng.standard_normal(2 * 2**20).astype(np.float64)                             # 16 MiB exactly
+    s.reset_counters()
+    hd = s.register_data(h.Data([a, b, c], h.DataKind.Generic))
+    assert s.counters() == {"host_to_device": 1, "device_to_host": 0}
+    got = s.fetch_data(hd).arrays
+    assert beq(got[0], a) and beq(got[1], b) and beq(got[2], c)
+    pinned = h.pinned_empty(b.shape, b.dtype)
+    pinned[...] = 0
+    out = s.fetch_data(hd, [np.empty_like(a), pinned, np.empty_like(c)]).arrays
+    assert beq(out[1], b) and beq(out[0], a) and beq(out[2], c)
+    hp = s.register_data(h.Data([pinned], h.DataKind.Generic))  # page-locked source: direct DMA
+    assert beq(s.fetch_data(hp).arrays[0], b)
+    s.release_data(hd)
+    s.release_data(hp)
