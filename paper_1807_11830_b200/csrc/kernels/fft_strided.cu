@@ -9,6 +9,10 @@ namespace {
 
 template <int N, int RQ>
 int strided_occ(int block, int smem, int variant) {
+    // the generic (non-square) instantiations run whatever the variant: give
+    // them the shared-memory attribute too
+    blocks_per_sm(k_fft_strided<N, -1, 0, RQ>, block, smem);
+    blocks_per_sm(k_fft_strided<N, 1, 0, RQ>, block, smem);
     if constexpr (has_variants<N>()) {
         if ((variant & 2) && !(variant & 1)) {
             blocks_per_sm(k_fft_strided<N, -1, N, RQ, false, 3>, block, smem);
@@ -67,8 +71,11 @@ LaunchShape plan_strided(std::uint64_t N, std::uint64_t nx, std::uint64_t planes
     const int R = points_for(N, rq);
     if (R == 0) return s;
     s.rq = R;
-    // bit 0 next-tile prefetch (512), bit 1 three CTAs per SM register cap (256)
-    s.variant = env_int("HETRECO_STRIDED_PF", N == 512 ? 1 : (N == 256 ? 2 : 0));
+    // bit 0 next-tile prefetch, bit 1 three CTAs per SM register cap.
+    // Measured on B200 (profiles/round1_summary.md): 256 -> 32-column tiles
+    // with next-tile prefetch (170 us vs 181 us for 16 columns under the
+    // 3-CTA register cap at C3); 512 -> 8-column tiles with prefetch.
+    s.variant = env_int("HETRECO_STRIDED_PF", (N == 512 || N == 256) ? 1 : 0);
     const int T = int(N) / R;
     const int ls_bytes = stride_of(N) * 8;
     // columns per tile: >= 16 (128-B rows) when possible, bounded by 512
@@ -76,7 +83,7 @@ LaunchShape plan_strided(std::uint64_t N, std::uint64_t nx, std::uint64_t planes
     std::uint64_t tx = std::max(16, 256 / T);
     tx = std::min<std::uint64_t>(tx, std::uint64_t(std::max(1, 512 / T)));
     tx = std::min<std::uint64_t>(tx, std::uint64_t(std::max(1, (100 * 1024) / ls_bytes)));
-    if (const int e = env_int("HETRECO_STRIDED_TX", N == 512 ? 8 : 0)) tx = std::uint64_t(e);
+    if (const int e = env_int("HETRECO_STRIDED_TX", N == 512 ? 8 : (N == 256 ? 32 : 0))) tx = std::uint64_t(e);
     tx = std::min<std::uint64_t>(tx, nx);
     while (tx > 1 && nx % tx) tx >>= 1;  // both powers of two in practice
     s.block = int(tx) * T;
