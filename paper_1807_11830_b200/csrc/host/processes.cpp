@@ -31,13 +31,13 @@ long env_or(const char* name, long fallback) {
 }
 
 // The staged-map SENSE combine (fft_combine_ss.cu) where it measured faster
-// (256^2 C3: 131 -> 121 us; 512^2: 162 -> 202 us, 160^2: even), unless
+// (256^2 C3: 131 -> 114 us; 512^2 x 8: 162 -> 159 us; 160^2: even), unless
 // HETRECO_COMBINE_SS=0 (off) / =1 (every supported size).
 bool combine_ss_enabled(std::uint64_t nx) {
     const char* e = std::getenv("HETRECO_COMBINE_SS");
     if (e && *e == '0') return false;
     if (!dev::combine_ss_supported(nx)) return false;
-    return (e && *e == '1') || (nx >= 64 && nx <= 256 && is_pow2(nx));
+    return (e && *e == '1') || (nx >= 64 && nx <= 512 && is_pow2(nx));
 }
 
 // Owning device allocation on the session's GPU.

@@ -6,8 +6,7 @@
 // 8 warps per SM, and the SENSE pass runs 30 % slower than the RSS pass that
 // reads no maps (profiles/round1_combine.md).  Here the LPB lines of a CTA are
 // one row y of LPB consecutive frames, so they share S[:, y, c]: the CTA
-// stages that 2 KB row into shared memory one coil ahead (2 loads per thread
-// at 256^2), every line reads it at the point of use, and the register budget
+// stages that row into shared memory one coil ahead, every line reads it at the point of use, and the register budget
 // drops to the transform + X prefetch + accumulators.  One bar.sync per coil.
 //
 // Same semantics as k_fft_combine's fp32 SENSE variant (complex_element_prod
@@ -19,7 +18,15 @@ namespace hetreco::dev {
 
 namespace {
 
+// Frames per CTA.  Measured at C3 shapes (profiles/round1_combine.md):
+// 256^2 -> 16: 168 us, 8: 121, 4: 114, 2: 113; 512^2 x 8 -> 8: 203, 4: 172,
+// 2: 159 (register-prefetch kernel 162).  HETRECO_SS_LINES = 2|4|8|16 overrides.
 constexpr int kSsLines = 8;
+
+int ss_lines(std::uint64_t N) {
+    const int v = env_int("HETRECO_SS_LINES", N >= 512 ? 2 : 4);
+    return (v == 2 || v == 4 || v == 8 || v == 16) ? v : kSsLines;
+}
 
 template <int N, int LPB>
 __global__ void __launch_bounds__(LPB * LineFFT<N>::T) k_fft_combine_ss(ContigArgs a, std::uint32_t gpy,
@@ -95,34 +102,56 @@ __global__ void __launch_bounds__(LPB * LineFFT<N>::T) k_fft_combine_ss(ContigAr
     }
 }
 
-template <int N>
+template <int N, int LPB>
 constexpr int ss_smem() {
-    return (kSsLines * line_stride<N>() + 2 * N) * 8;
+    return (LPB * line_stride<N>() + 2 * N) * 8;
 }
 
-template <int n>
-LaunchShape plan_ss_n(std::uint64_t ny, std::uint64_t frames, int sms) {
+template <int n, int LPB>
+LaunchShape plan_ss_nl(std::uint64_t ny, std::uint64_t frames, int sms) {
     LaunchShape s;
-    if constexpr (n >= 64) {
+    if constexpr (n >= 64 && LPB * LineFFT<n>::T <= 1024) {
         s.rq = LineFFT<n>::R;
-        s.block = kSsLines * LineFFT<n>::T;
-        s.smem = ss_smem<n>();
-        const std::uint64_t groups = ny * ((frames + kSsLines - 1) / kSsLines);
-        const int occ = blocks_per_sm(k_fft_combine_ss<n, kSsLines>, s.block, s.smem);
+        s.block = LPB * LineFFT<n>::T;
+        s.smem = ss_smem<n, LPB>();
+        const std::uint64_t groups = ny * ((frames + LPB - 1) / LPB);
+        const int occ = blocks_per_sm(k_fft_combine_ss<n, LPB>, s.block, s.smem);
         s.grid = int(std::min<std::uint64_t>(groups, std::uint64_t(sms) * occ));
-        s.variant = 256;
+        s.variant = 256 | (LPB << 10);
     }
     return s;
 }
 
 template <int n>
-cudaError_t launch_ss_n(const ContigArgs& a, const LaunchShape& s, std::uint32_t gpy, std::uint32_t groups,
-                        cudaStream_t st) {
-    if constexpr (n >= 64) {
-        k_fft_combine_ss<n, kSsLines><<<s.grid, s.block, s.smem, st>>>(a, gpy, groups);
+LaunchShape plan_ss_n(std::uint64_t ny, std::uint64_t frames, int sms) {
+    switch (ss_lines(std::uint64_t(n))) {
+        case 2: return plan_ss_nl<n, 2>(ny, frames, sms);
+        case 4: return plan_ss_nl<n, 4>(ny, frames, sms);
+        case 16: return plan_ss_nl<n, 16>(ny, frames, sms);
+        default: return plan_ss_nl<n, 8>(ny, frames, sms);
+    }
+}
+
+template <int n, int LPB>
+cudaError_t launch_ss_nl(const ContigArgs& a, const LaunchShape& s, cudaStream_t st) {
+    if constexpr (n >= 64 && LPB * LineFFT<n>::T <= 1024) {
+        const std::uint64_t gpy = (a.frames + LPB - 1) / LPB;
+        const std::uint64_t groups = a.ny * gpy;
+        if (groups >= (std::uint64_t(1) << 32)) return cudaErrorInvalidValue;
+        k_fft_combine_ss<n, LPB><<<s.grid, s.block, s.smem, st>>>(a, std::uint32_t(gpy), std::uint32_t(groups));
         return cudaGetLastError();
     } else {
         return cudaErrorInvalidValue;
+    }
+}
+
+template <int n>
+cudaError_t launch_ss_n(const ContigArgs& a, const LaunchShape& s, cudaStream_t st) {
+    switch (s.variant >> 10) {
+        case 2: return launch_ss_nl<n, 2>(a, s, st);
+        case 4: return launch_ss_nl<n, 4>(a, s, st);
+        case 16: return launch_ss_nl<n, 16>(a, s, st);
+        default: return launch_ss_nl<n, 8>(a, s, st);
     }
 }
 
@@ -152,12 +181,9 @@ LaunchShape plan_combine_ss(std::uint64_t N, std::uint64_t ny, std::uint64_t fra
 
 cudaError_t launch_combine_ss(std::uint64_t N, const ContigArgs& a, const LaunchShape& s, cudaStream_t st) {
     if (s.block == 0 || !(s.variant & 256)) return cudaErrorInvalidValue;
-    const std::uint64_t gpy = (a.frames + kSsLines - 1) / kSsLines;
-    const std::uint64_t groups = a.ny * gpy;
-    if (groups >= (std::uint64_t(1) << 32)) return cudaErrorInvalidValue;
     switch (N) {
 #define X(n) \
-    case n: return launch_ss_n<n>(a, s, std::uint32_t(gpy), std::uint32_t(groups), st);
+    case n: return launch_ss_n<n>(a, s, st);
         HETRECO_FFT_SIZES(X)
 #undef X
     }
