@@ -101,11 +101,19 @@ def dist_setup(n_gpus: int):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # HETRECO_BENCH_DEVICE pins every rank to one GPU (with
+    # HETRECO_BENCH_DIST=gloo): a dry run of the multi-rank path on a 1-GPU box
+    if os.environ.get("HETRECO_BENCH_DEVICE"):
+        local = int(os.environ["HETRECO_BENCH_DEVICE"])
     if world > 1:
         import torch
         import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("HETRECO_BENCH_DIST", "nccl")
+        if backend == "nccl":
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     return rank, world, local
 
 
