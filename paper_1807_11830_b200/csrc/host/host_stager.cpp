@@ -20,6 +20,13 @@ void ck(cudaError_t e, const char* what) {
 
 // ---- CopyPool -----------------------------------------------------------------------------
 
+namespace {
+// Bytes per part, rounded up to a cache line; parts * result >= n for every n.
+std::size_t part_bytes(std::size_t n, unsigned parts) {
+    return ((n + parts - 1) / parts + 63) & ~std::size_t(63);
+}
+}  // namespace
+
 CopyPool::CopyPool(unsigned threads) {
     for (unsigned i = 1; i < std::max(1u, threads); ++i) workers_.emplace_back([this, i] { run(i); });
 }
@@ -50,7 +57,7 @@ void CopyPool::run(unsigned index) {
             n = n_;
         }
         const unsigned parts = size();
-        const std::size_t per = (n / parts + 63) & ~std::size_t(63);
+        const std::size_t per = part_bytes(n, parts);
         const std::size_t b = std::min(n, per * index), e = std::min(n, b + per);
         if (e > b) std::memcpy(d + b, s + b, e - b);
         {
@@ -75,7 +82,7 @@ void CopyPool::copy(void* dst, const void* src, std::size_t n) {
     }
     go_.notify_all();
     const unsigned parts = size();
-    const std::size_t per = (n / parts + 63) & ~std::size_t(63);
+    const std::size_t per = part_bytes(n, parts);
     std::memcpy(dst, src, std::min(n, per));  // the caller's share (part 0)
     std::unique_lock lk(mu_);
     done_.wait(lk, [&] { return pending_ == 0; });

@@ -687,6 +687,11 @@ def test_large_pageable_transfers_through_staging_ring(s):
     a = rng.integers(0, 255, 5 * 2**20 + 13, dtype=np.uint8)
     b = np.asfortranarray(rng.standard_normal((1031, 977, 5)).astype(np.complex64))   # ~38 MiB
     c = rng.standard_normal(2 * 2**20).astype(np.float64)                             # 16 MiB exactly
+    # floor(n / parts) a multiple of 64 with a remainder, for every pool size 2..8
+    d = rng.integers(0, 255, 840 * 64 * 79 + 1, dtype=np.uint8)
+    hdd = s.register_data(h.Data([d], h.DataKind.Generic))
+    assert beq(s.fetch_data(hdd).arrays[0], d)
+    s.release_data(hdd)
     s.reset_counters()
     hd = s.register_data(h.Data([a, b, c], h.DataKind.Generic))
     assert s.counters() == {"host_to_device": 1, "device_to_host": 0}
