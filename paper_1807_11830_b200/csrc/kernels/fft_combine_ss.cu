@@ -116,7 +116,8 @@ LaunchShape plan_ss_nl(std::uint64_t ny, std::uint64_t frames, int sms) {
         s.smem = ss_smem<n, LPB>();
         const std::uint64_t groups = ny * ((frames + LPB - 1) / LPB);
         const int occ = blocks_per_sm(k_fft_combine_ss<n, LPB>, s.block, s.smem);
-        s.grid = int(std::min<std::uint64_t>(groups, std::uint64_t(sms) * occ));
+        const int per_sm = env_int("HETRECO_SS_CTAS_PER_SM", occ);  // experiments (profiles/round1_combine.md)
+        s.grid = int(std::min<std::uint64_t>(groups, std::uint64_t(sms) * std::uint64_t(per_sm > 0 ? per_sm : occ)));
         s.variant = 256 | (LPB << 10);
     }
     return s;
