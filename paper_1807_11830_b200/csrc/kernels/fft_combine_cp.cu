@@ -35,8 +35,17 @@ constexpr int cp_groups() {  // coil groups per CTA: ~128 threads
     return T >= 128 ? 1 : 128 / T;
 }
 
+// Resident-CTA floor (a 128-register cap) for the 20-point lines of 5*2^k
+// SENSE: uncapped they take 254 registers (2 CTAs/SM).  Measured at C3 shapes
+// (profiles/round1_combine.md): 160^2 160 -> 150 us; the cap slows RSS and the
+// 12-point 3*2^k lines, which keep the default.
+template <int N, int MODE>
+constexpr int cp_min_blocks() {
+    return (odd_part(N) == 5 && MODE == int(Combine::Sense)) ? 4 : 0;
+}
+
 template <int N, int MODE, int G>
-__global__ void __launch_bounds__(G * LineFFT<N>::T) k_fft_combine_cp(ContigArgs a, std::uint32_t items) {
+__global__ void __launch_bounds__(G * LineFFT<N>::T, cp_min_blocks<N, MODE>()) k_fft_combine_cp(ContigArgs a, std::uint32_t items) {
     using L = LineFFT<N>;
     constexpr int R = L::R, T = L::T;
     constexpr bool SENSE = MODE == int(Combine::Sense);
@@ -65,12 +74,18 @@ __global__ void __launch_bounds__(G * LineFFT<N>::T) k_fft_combine_cp(ContigArgs
             float2 v[R];
             const float2* src = xbase + c * coil_stride;
             slots_ld<R>(sh_in, (long long)(R / 2) * T, [&](auto m, long long d) { v[m.value] = __ldcs(src + T * m.value + d); });
+            // map row: issued before the transform (in flight during it) for
+            // powers of two; at the point of use for mixed radix, whose 20-point
+            // threads cannot hold another R registers across the transform
+            constexpr bool kEarlyMap = !is_mixed_size(N);
             float2 sv[SENSE ? R : 1];
-            if constexpr (SENSE) {
-                const float2* sp = sbase + c * coil_stride;
+            const float2* sp = sbase + c * coil_stride;
+            auto load_map = [&] {
                 slots_ld<R>(sh_out, (long long)(R / 2) * T, [&](auto m, long long d) { sv[m.value] = __ldg(sp + T * m.value + d); });
-            }
+            };
+            if constexpr (SENSE && kEarlyMap) load_map();
             L::template run<+1>(v, tw, line, j, [mask] { __syncwarp(mask); }, a.scale);
+            if constexpr (SENSE && !kEarlyMap) load_map();
             if constexpr (SENSE) {
                 sfor<R>([&](auto m) { mac_conj(acc_re[m.value], acc_im[m.value], v[m.value], sv[m.value]); });
             } else {
