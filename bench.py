@@ -248,7 +248,7 @@ def run_ours(args):
     kernels = [
         {"name": "k_fft_strided<256,+1,256,16,PF> (axis-1 IFFT, 32-column tiles, next-tile prefetch)", "seconds": k_axis1, "bytes": bytes_axis1,
          "gbs": bytes_axis1 / k_axis1 / 1e9},
-        {"name": "k_fft_combine_ss<256,8> (axis-0 IFFT + conj(S) coil combine, map rows staged in smem)",
+        {"name": "k_fft_combine_ss<256,4> (axis-0 IFFT + conj(S) coil combine, map rows staged in smem)",
          "seconds": k_axis0,
          "bytes": bytes_axis0, "gbs": bytes_axis0 / k_axis0 / 1e9},
     ]
