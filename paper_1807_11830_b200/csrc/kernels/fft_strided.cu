@@ -7,6 +7,126 @@ bool fft_size_supported(std::uint64_t n) { return points_for(n, 0) != 0; }
 
 namespace {
 
+// ---- column tiles through a shared-memory ring (512-point columns, default) ----
+//
+// At 512^2 the register-prefetch kernel holds one 512-thread CTA per SM
+// (8 columns x 64 threads, 96 registers): ~32 KB per SM in flight in 64-byte
+// row segments, 0.63 of the HBM peak (profiles/round1_summary.md).  Here the
+// CTA keeps K-1 column tiles in flight with cp.async (16-byte chunks,
+// row-major [N rows][TX columns] per stage), then each thread reads its
+// column samples from the landed stage and runs the same transform and
+// stores as k_fft_strided -- bit-identical output.  Square images only.
+// Default: 16 columns (128-byte row segments), 2 stages, 1024 threads.
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(static_cast<std::uint32_t>(__cvta_generic_to_shared(dst))),
+                 "l"(src)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int PENDING>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(PENDING) : "memory");
+}
+
+template <int N, int DIR, int RQ, int K, int TX>
+__global__ void __launch_bounds__(TX * (N / RQ)) k_fft_strided_ring(StridedArgs a, std::uint32_t ntiles) {
+    using L = LineFFT<N, RQ>;
+    constexpr int R = L::R, T = L::T, NT = TX * T;
+    constexpr int TILE = N * TX;        // float2 per stage
+    constexpr int CPR = TX / 2;         // 16-byte chunks per tile row
+    extern __shared__ __align__(16) float2 smem[];
+    const int tid = threadIdx.x;
+    const int l = tid % TX, j = tid / TX;
+    float2* ring = smem;
+    float2* line = smem + K * TILE + l * line_stride<N>();
+    typename L::Twiddles tw;
+    L::load_twiddles(tw, a.tw, j, a.scale);
+    constexpr std::uint32_t nx = N, xtiles = N / TX;
+    constexpr std::uint64_t plane_elems = std::uint64_t(N) * N;
+    const bool sh_in = a.shift_in, sh_out = a.shift_out;
+    auto tile_base = [&](std::uint32_t tile) {
+        const std::uint32_t plane = tile / xtiles, xt = tile % xtiles;
+        return std::uint64_t(plane) * plane_elems + xt * std::uint32_t(TX);
+    };
+    auto issue = [&](std::uint32_t tile, int stage) {
+        if (tile < ntiles) {
+            const float2* src = a.in + tile_base(tile);
+            float2* dst = ring + stage * TILE;
+            sfor<N * CPR / NT>([&](auto k) {
+                const int q = tid + k.value * NT;
+                const int row = q / CPR, cc = q % CPR;
+                cp_async16(dst + row * TX + 2 * cc, src + std::uint64_t(row) * nx + 2 * cc);
+            });
+        }
+        cp_async_commit();
+    };
+    std::uint32_t tile = blockIdx.x;
+    sfor<K - 1>([&](auto k) { issue(tile + std::uint32_t(k.value) * gridDim.x, k.value); });
+    for (int i = 0; tile < ntiles; ++i, tile += gridDim.x) {
+        const int stage = i % K;
+        cp_async_wait<K - 2>();
+        __syncthreads();  // stage landed for every thread; stage i-1 free
+        issue(tile + std::uint32_t(K - 1) * gridDim.x, (i + K - 1) % K);
+        const float2* t = ring + stage * TILE + l;
+        float2 v[R];
+        slots_ld<R>(sh_in, (long long)(R / 2) * T,
+                    [&](auto m, long long d) { v[m.value] = t[(j + T * m.value + int(d)) * TX]; });
+        L::template run<DIR>(v, tw, line, j, [] { __syncthreads(); }, a.scale);
+        float2* dst = a.out + tile_base(tile) + l + std::uint32_t(j) * nx;
+        slots<R>(sh_out, [&](auto m, auto ms) { dst[ms.value * T * N] = v[m.value]; });
+    }
+    cp_async_wait<0>();
+}
+
+// Stages K and columns per tile.  Measured at 512^2 x 32 coils x 8 frames
+// (profiles/round1_summary.md), axis-1 us: register prefetch 260; 8 columns
+// with K = 3/4/5 stages 252/240/240; 16 columns (128-byte row segments,
+// 1024 threads, 64 registers) with K = 2: 187 -- the default.
+// HETRECO_STRIDED_RING = 0 selects the register-prefetch kernel.
+int ring_tx(int K) {
+    const int tx = env_int("HETRECO_RING_TX", 16);
+    if (tx == 16) return K == 2 ? 16 : 0;
+    return (K >= 3 && K <= 5) ? 8 : 0;
+}
+
+int ring_smem_bytes(int K, int tx) { return (K * 512 * tx + tx * line_stride<512>()) * 8; }
+
+int ring_stages() { return env_int("HETRECO_STRIDED_RING", 2); }
+
+template <int N, int RQ, int K, int TX>
+int ring_occ_k(int block, int smem) {
+    return std::max(blocks_per_sm(k_fft_strided_ring<N, 1, RQ, K, TX>, block, smem),
+                    blocks_per_sm(k_fft_strided_ring<N, -1, RQ, K, TX>, block, smem));
+}
+
+template <int N, int RQ>
+int ring_occ(int K, int tx, int block, int smem) {
+    if (tx == 16) return ring_occ_k<N, RQ, 2, 16>(block, smem);
+    switch (K) {
+        case 3: return ring_occ_k<N, RQ, 3, 8>(block, smem);
+        case 4: return ring_occ_k<N, RQ, 4, 8>(block, smem);
+        default: return ring_occ_k<N, RQ, 5, 8>(block, smem);
+    }
+}
+
+template <int N, int RQ, int K, int TX>
+void ring_launch(int dir, const StridedArgs& a, const LaunchShape& s, std::uint32_t tiles, cudaStream_t st) {
+    if (dir > 0)
+        k_fft_strided_ring<N, 1, RQ, K, TX><<<s.grid, s.block, s.smem, st>>>(a, tiles);
+    else
+        k_fft_strided_ring<N, -1, RQ, K, TX><<<s.grid, s.block, s.smem, st>>>(a, tiles);
+}
+
+template <int N, int RQ>
+void ring_go(int dir, int K, int tx, const StridedArgs& a, const LaunchShape& s, std::uint32_t tiles, cudaStream_t st) {
+    if (tx == 16) return ring_launch<N, RQ, 2, 16>(dir, a, s, tiles, st);
+    switch (K) {
+        case 3: return ring_launch<N, RQ, 3, 8>(dir, a, s, tiles, st);
+        case 4: return ring_launch<N, RQ, 4, 8>(dir, a, s, tiles, st);
+        default: return ring_launch<N, RQ, 5, 8>(dir, a, s, tiles, st);
+    }
+}
+
 template <int N, int RQ>
 int strided_occ(int block, int smem, int variant) {
     // the generic (non-square) instantiations run whatever the variant: give
@@ -32,6 +152,12 @@ int strided_occ(int block, int smem, int variant) {
 template <int N, int RQ>
 void strided_go(int dir, bool sq, const StridedArgs& a, const LaunchShape& s, int tx, std::uint32_t tiles,
                 cudaStream_t st) {
+    if constexpr (N == 512 && RQ == 8) {
+        if (sq && (s.variant & 4)) {
+            ring_go<N, RQ>(dir, (s.variant >> 3) & 7, tx, a, s, tiles, st);
+            return;
+        }
+    }
     if constexpr (has_variants<N>()) {
         if (sq && (s.variant & 2) && !(s.variant & 1)) {  // 3 CTAs/SM register cap
             if (dir > 0)
@@ -93,6 +219,17 @@ LaunchShape plan_strided(std::uint64_t N, std::uint64_t nx, std::uint64_t planes
     s.smem = int(tx) * ls_bytes;
     const std::uint64_t tiles = (nx / tx) * planes;
     int occ = 1;
+    if (const int K = ring_stages(); K && N == 512 && R == 8 && nx == 512) {
+        const int rtx = ring_tx(K);
+        if (rtx) {
+            s.variant = 4 | (K << 3);
+            s.block = rtx * T;
+            s.smem = ring_smem_bytes(K, rtx);
+            occ = ring_occ<512, 8>(K, rtx, s.block, s.smem);
+            s.grid = int(std::min<std::uint64_t>((nx / std::uint64_t(rtx)) * planes, std::uint64_t(sms) * occ));
+            return s;
+        }
+    }
     switch (N) {
 #define X(n)                                                              \
     case n:                                                               \

@@ -642,6 +642,29 @@ def test_staged_map_combine(s, monkeypatch, nx, ny, nc, nf, shift):
     assert relmax(M, ref) <= TOL
 
 
+@pytest.mark.parametrize("stages", ["3", "4", "5", "2x16"])
+@pytest.mark.parametrize("shift", [False, True])
+def test_strided_ring_512(s, monkeypatch, stages, shift):
+    """512-point axis-1 pass through the cp.async shared-memory ring
+    (k_fft_strided_ring): bit-identical to the register-prefetch pass for
+    fft2d both directions and the SENSE chain (partial last wave of tiles)."""
+    rng = np.random.default_rng(512 + len(stages))
+    Y = cplx(rng, 512, 512, 3, 5)
+    S = cplx(rng, 512, 512, 3)
+    k, _, tx = stages.partition("x")  # "2x16" is the default configuration
+    monkeypatch.setenv("HETRECO_RING_TX", tx or "8")
+    outs = {}
+    for ring in ("0", k):
+        monkeypatch.setenv("HETRECO_STRIDED_RING", ring)
+        (M,), _ = run_process(s, "sens_recon", [Y, S], [((512, 512, 5), np.complex64)], {"shift": shift})
+        x = Y[:, :, :, 0]
+        (fw,), _ = run_process(s, "fft2d", [x], [(x.shape, np.complex64)], {"direction": "forward", "shift": shift})
+        (bw,), _ = run_process(s, "fft2d", [x], [(x.shape, np.complex64)], {"direction": "inverse", "shift": shift})
+        outs[ring] = (M, fw, bw)
+    for a, b in zip(outs["0"], outs[k]):
+        assert beq(a, b)
+
+
 @pytest.mark.parametrize("method", ["sens_recon", "rss_recon"])
 def test_recon_overlap_pipeline_bitexact(s, method):
     """"overlap": true -- chunked axis-1/combine graph branches (fork/join over a
