@@ -246,7 +246,7 @@ def run_ours(args):
     bytes_axis0 = FRAME_Y * NF + SMAP + FRAME_M * NF  # read X + S, write M
     peak, peak_kind = peaks()
     kernels = [
-        {"name": "k_fft_strided<256,+1,256,16,PF> (axis-1 IFFT, 32-column tiles, next-tile prefetch)", "seconds": k_axis1, "bytes": bytes_axis1,
+        {"name": "k_fft_strided_ring<256,+1,16,2,32> (axis-1 IFFT, 32-column tiles through a 2-stage cp.async shared-memory ring)", "seconds": k_axis1, "bytes": bytes_axis1,
          "gbs": bytes_axis1 / k_axis1 / 1e9},
         {"name": "k_fft_combine_ss<256,4> (axis-0 IFFT + conj(S) coil combine, map rows staged in smem)",
          "seconds": k_axis0,

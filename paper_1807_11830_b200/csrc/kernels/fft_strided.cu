@@ -7,7 +7,7 @@ bool fft_size_supported(std::uint64_t n) { return points_for(n, 0) != 0; }
 
 namespace {
 
-// ---- column tiles through a shared-memory ring (512-point columns, default) ----
+// ---- column tiles through a shared-memory ring (256/512-point columns, default) ----
 //
 // At 512^2 the register-prefetch kernel holds one 512-thread CTA per SM
 // (8 columns x 64 threads, 96 registers): ~32 KB per SM in flight in 64-byte
@@ -16,7 +16,8 @@ namespace {
 // row-major [N rows][TX columns] per stage), then each thread reads its
 // column samples from the landed stage and runs the same transform and
 // stores as k_fft_strided -- bit-identical output.  Square images only.
-// Default: 16 columns (128-byte row segments), 2 stages, 1024 threads.
+// Default: 16 columns (128-byte row segments), 2 stages, 1024 threads at
+// 512^2; 32 columns, 2 stages, 512 threads at 256^2.
 __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(static_cast<std::uint32_t>(__cvta_generic_to_shared(dst))),
                  "l"(src)
@@ -78,11 +79,12 @@ __global__ void __launch_bounds__(TX * (N / RQ)) k_fft_strided_ring(StridedArgs 
     cp_async_wait<0>();
 }
 
-// Stages K and columns per tile.  Measured at 512^2 x 32 coils x 8 frames
-// (profiles/round1_summary.md), axis-1 us: register prefetch 260; 8 columns
+// Stages K and columns per tile.  Measured (profiles/round1_summary.md),
+// axis-1 us at 512^2 x 32 coils x 8 frames: register prefetch 260; 8 columns
 // with K = 3/4/5 stages 252/240/240; 16 columns (128-byte row segments,
-// 1024 threads, 64 registers) with K = 2: 187 -- the default.
-// HETRECO_STRIDED_RING = 0 selects the register-prefetch kernel.
+// 1024 threads, 64 registers) with K = 2: 187 -- the default.  At 256^2 C3:
+// register prefetch 173, 32 columns x 2 stages (512 threads) 160-163 -- the
+// default.  HETRECO_STRIDED_RING = 0 selects the register-prefetch kernel.
 int ring_tx(int K) {
     const int tx = env_int("HETRECO_RING_TX", 16);
     if (tx == 16) return K == 2 ? 16 : 0;
@@ -158,6 +160,12 @@ void strided_go(int dir, bool sq, const StridedArgs& a, const LaunchShape& s, in
             return;
         }
     }
+    if constexpr (N == 256 && RQ == 16) {
+        if (sq && (s.variant & 4)) {
+            ring_launch<N, RQ, 2, 32>(dir, a, s, tiles, st);
+            return;
+        }
+    }
     if constexpr (has_variants<N>()) {
         if (sq && (s.variant & 2) && !(s.variant & 1)) {  // 3 CTAs/SM register cap
             if (dir > 0)
@@ -219,6 +227,14 @@ LaunchShape plan_strided(std::uint64_t N, std::uint64_t nx, std::uint64_t planes
     s.smem = int(tx) * ls_bytes;
     const std::uint64_t tiles = (nx / tx) * planes;
     int occ = 1;
+    if (N == 256 && R == 16 && nx == 256 && ring_stages()) {  // 32 columns (256-B rows), 2 stages
+        s.variant = 4 | (2 << 3);
+        s.block = 32 * T;
+        s.smem = (2 * 256 * 32 + 32 * line_stride<256>()) * 8;
+        occ = ring_occ_k<256, 16, 2, 32>(s.block, s.smem);
+        s.grid = int(std::min<std::uint64_t>((nx / 32) * planes, std::uint64_t(sms) * occ));
+        return s;
+    }
     if (const int K = ring_stages(); K && N == 512 && R == 8 && nx == 512) {
         const int rtx = ring_tx(K);
         if (rtx) {

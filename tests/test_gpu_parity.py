@@ -642,21 +642,21 @@ def test_staged_map_combine(s, monkeypatch, nx, ny, nc, nf, shift):
     assert relmax(M, ref) <= TOL
 
 
-@pytest.mark.parametrize("stages", ["3", "4", "5", "2x16"])
+@pytest.mark.parametrize("n,stages", [(512, "3"), (512, "4"), (512, "5"), (512, "2x16"), (256, "2")])
 @pytest.mark.parametrize("shift", [False, True])
-def test_strided_ring_512(s, monkeypatch, stages, shift):
-    """512-point axis-1 pass through the cp.async shared-memory ring
+def test_strided_ring(s, monkeypatch, n, stages, shift):
+    """256/512-point axis-1 pass through the cp.async shared-memory ring
     (k_fft_strided_ring): bit-identical to the register-prefetch pass for
     fft2d both directions and the SENSE chain (partial last wave of tiles)."""
-    rng = np.random.default_rng(512 + len(stages))
-    Y = cplx(rng, 512, 512, 3, 5)
-    S = cplx(rng, 512, 512, 3)
+    rng = np.random.default_rng(n + len(stages))
+    Y = cplx(rng, n, n, 3, 5)
+    S = cplx(rng, n, n, 3)
     k, _, tx = stages.partition("x")  # "2x16" is the default configuration
     monkeypatch.setenv("HETRECO_RING_TX", tx or "8")
     outs = {}
     for ring in ("0", k):
         monkeypatch.setenv("HETRECO_STRIDED_RING", ring)
-        (M,), _ = run_process(s, "sens_recon", [Y, S], [((512, 512, 5), np.complex64)], {"shift": shift})
+        (M,), _ = run_process(s, "sens_recon", [Y, S], [((n, n, 5), np.complex64)], {"shift": shift})
         x = Y[:, :, :, 0]
         (fw,), _ = run_process(s, "fft2d", [x], [(x.shape, np.complex64)], {"direction": "forward", "shift": shift})
         (bw,), _ = run_process(s, "fft2d", [x], [(x.shape, np.complex64)], {"direction": "inverse", "shift": shift})
