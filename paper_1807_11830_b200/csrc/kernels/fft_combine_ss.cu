@@ -25,7 +25,7 @@ constexpr int kSsLines = 8;
 
 int ss_lines(std::uint64_t N) {
     const int v = env_int("HETRECO_SS_LINES", N >= 512 ? 2 : 4);
-    return (v == 2 || v == 4 || v == 8 || v == 16) ? v : kSsLines;
+    return (v == 2 || v == 4 || v == 6 || v == 8 || v == 16) ? v : kSsLines;
 }
 
 template <int N, int LPB>
@@ -128,6 +128,7 @@ LaunchShape plan_ss_n(std::uint64_t ny, std::uint64_t frames, int sms) {
     switch (ss_lines(std::uint64_t(n))) {
         case 2: return plan_ss_nl<n, 2>(ny, frames, sms);
         case 4: return plan_ss_nl<n, 4>(ny, frames, sms);
+        case 6: return plan_ss_nl<n, 6>(ny, frames, sms);
         case 16: return plan_ss_nl<n, 16>(ny, frames, sms);
         default: return plan_ss_nl<n, 8>(ny, frames, sms);
     }
@@ -151,6 +152,7 @@ cudaError_t launch_ss_n(const ContigArgs& a, const LaunchShape& s, cudaStream_t 
     switch (s.variant >> 10) {
         case 2: return launch_ss_nl<n, 2>(a, s, st);
         case 4: return launch_ss_nl<n, 4>(a, s, st);
+        case 6: return launch_ss_nl<n, 6>(a, s, st);
         case 16: return launch_ss_nl<n, 16>(a, s, st);
         default: return launch_ss_nl<n, 8>(a, s, st);
     }
