@@ -219,15 +219,25 @@ LaunchShape plan_strided(std::uint64_t N, std::uint64_t nx, std::uint64_t planes
     tx = std::min<std::uint64_t>(tx, std::uint64_t(std::max(1, (100 * 1024) / ls_bytes)));
     // mixed-radix columns (8 threads each): 16-column tiles (160^2 C3: 91 vs 97 us at 32)
     const bool mixed = (N & (N - 1)) != 0;
-    if (const int e = env_int("HETRECO_STRIDED_TX", N == 512 ? 8 : (N == 256 ? 32 : (mixed ? 16 : 0))))
-        tx = std::uint64_t(e);
+    // Few planes (C2: 256^2 x 8 coils x 1 frame = 64 wide tiles for 148 SMs):
+    // narrower tiles without prefetch or ring fill more SMs (C2 axis-1 kernel
+    // 11.1 -> 9.9 us with 16 columns).
+    const int ring_cols = N == 256 ? 32 : (N == 512 ? 16 : 0);
+    const bool few_tiles = ring_cols && nx == N && (nx / std::uint64_t(ring_cols)) * planes < std::uint64_t(sms);
+    int tx_default = N == 512 ? 8 : (N == 256 ? 32 : (mixed ? 16 : 0));
+    if (few_tiles) {
+        tx_default = 16;
+        while (tx_default > 8 && (nx / std::uint64_t(tx_default)) * planes < std::uint64_t(sms)) tx_default >>= 1;
+        s.variant = env_int("HETRECO_STRIDED_PF", 0);
+    }
+    if (const int e = env_int("HETRECO_STRIDED_TX", tx_default)) tx = std::uint64_t(e);
     tx = std::min<std::uint64_t>(tx, nx);
     while (tx > 1 && nx % tx) tx >>= 1;  // both powers of two in practice
     s.block = int(tx) * T;
     s.smem = int(tx) * ls_bytes;
     const std::uint64_t tiles = (nx / tx) * planes;
     int occ = 1;
-    if (N == 256 && R == 16 && nx == 256 && ring_stages()) {  // 32 columns (256-B rows), 2 stages
+    if (N == 256 && R == 16 && nx == 256 && ring_stages() && !few_tiles) {  // 32 columns (256-B rows), 2 stages
         s.variant = 4 | (2 << 3);
         s.block = 32 * T;
         s.smem = (2 * 256 * 32 + 32 * line_stride<256>()) * 8;
@@ -235,7 +245,7 @@ LaunchShape plan_strided(std::uint64_t N, std::uint64_t nx, std::uint64_t planes
         s.grid = int(std::min<std::uint64_t>((nx / 32) * planes, std::uint64_t(sms) * occ));
         return s;
     }
-    if (const int K = ring_stages(); K && N == 512 && R == 8 && nx == 512) {
+    if (const int K = ring_stages(); K && N == 512 && R == 8 && nx == 512 && !few_tiles) {
         const int rtx = ring_tx(K);
         if (rtx) {
             s.variant = 4 | (K << 3);
