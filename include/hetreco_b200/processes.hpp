@@ -156,7 +156,7 @@ private:
 // process.hpp:122-140
 class CompositeProcess : public GraphProcess {
 public:
-    CompositeProcess(ComputeSession& session, std::string name, std::vector<std::unique_ptr<Process>> stages);
+    CompositeProcess(ComputeSession& session, std::string name, std::vector<std::unique_ptr<Process>>&& stages);
     std::size_t stage_count() const { return stages_.size(); }
     Process& stage(std::size_t i) { return *stages_.at(i); }
     void record(cudaStream_t stream) override;
@@ -171,8 +171,9 @@ private:
     bool all_graph_ = true;
 };
 
+// On failure (ChainMismatch, InvalidArgument) the stages stay in `stages`.
 std::unique_ptr<CompositeProcess> chain(ComputeSession& session, std::string name,
-                                        std::vector<std::unique_ptr<Process>> stages);
+                                        std::vector<std::unique_ptr<Process>>&& stages);
 
 // ---- builtin processes ------------------------------------------------
 

@@ -11,6 +11,7 @@
 // throws NoMatchingDevice.
 #pragma once
 
+#include <atomic>
 #include <compare>
 #include <cstdint>
 #include <map>
@@ -197,12 +198,21 @@ public:
     void* device_pointer(BufferId buffer) const;       // base of the allocation
     std::uint64_t buffer_size(BufferId buffer) const;
     std::uint64_t live_bytes() const;
-    cudaStream_t compute_stream() const { return compute_; }
-    cudaStream_t h2d_stream() const { return h2d_; }
-    cudaStream_t d2h_stream() const { return d2h_; }
-    void make_current() const;                         // cudaSetDevice(ordinal)
+    cudaStream_t compute_stream() const { ensure(); return compute_; }
+    cudaStream_t h2d_stream() const { ensure(); return h2d_; }
+    cudaStream_t d2h_stream() const { ensure(); return d2h_; }
+    void make_current() const;                         // ensure() + cudaSetDevice(ordinal)
+    // Creates the device state (context, streams, params ring) on first use.
+    void ensure() const;
+    bool initialized() const { return ready_.load(std::memory_order_acquire); }
     // Raises DeviceError(last kernel) if the device reported a fault.
     void check(const char* what) const;
+    // Sequence number of work enqueued on the compute stream: every enqueue
+    // (backend entry points, process launches, streaming, phantom) bumps it,
+    // so LaunchStats can tell whether a launch was queued directly behind the
+    // same process' previous launch.
+    std::uint64_t work_seq() const { return work_seq_.load(std::memory_order_relaxed); }
+    void note_work() const { work_seq_.fetch_add(1, std::memory_order_relaxed); }
 
 private:
     struct Buf {
@@ -220,13 +230,15 @@ private:
     mutable std::mutex mu_;
     std::unordered_map<BufferId, Buf> bufs_;
     BufferId next_ = 1;
+    mutable std::mutex init_mu_;
+    mutable std::atomic<bool> ready_{false};
     cudaStream_t compute_ = nullptr, h2d_ = nullptr, d2h_ = nullptr;
-    cudaEvent_t ev_compute_ = nullptr, ev_copy_ = nullptr;
     // params staging ring (pinned host -> device), recycled after a sync
     std::byte* ring_host_ = nullptr;
     std::byte* ring_dev_ = nullptr;
     std::uint64_t ring_size_ = 0, ring_head_ = 0;
     mutable std::string last_kernel_;
+    mutable std::atomic<std::uint64_t> work_seq_{0};
     // pageable host <-> device transfers through a pinned ring (lazily built)
     mutable std::unique_ptr<detail::HostStager> stager_;
     detail::HostStager& stager() const;

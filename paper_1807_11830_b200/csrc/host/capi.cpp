@@ -510,28 +510,44 @@ int hetreco_process_create(hetreco_session s, const char* kind, const char* name
 int hetreco_chain_create(hetreco_session s, const char* name, hetreco_process* stages, int n, hetreco_process* out) {
     return guard([&] {
         need(out, "out");
-        std::vector<std::unique_ptr<Process>> v;
+        need(s, "session");
+        if (n <= 0) throw InvalidArgument("chain needs at least one stage");
+        need(stages, "stages");
+        // Validate everything before ownership moves, so any failure leaves
+        // the caller's stage handles intact: owned stages of this session,
+        // each handle once, and stage i's output feeding stage i + 1.
         for (int i = 0; i < n; ++i) {
             need(stages[i], "stage");
             if (!stages[i]->owned) throw InvalidArgument("chain stage " + std::to_string(i) + " is not owned");
+            if (&stages[i]->p->session() != s->s.get())
+                throw ChainMismatch("stage " + std::to_string(i) + " belongs to another session");
+            for (int k = 0; k < i; ++k)
+                if (stages[k] == stages[i])
+                    throw InvalidArgument("chain stage handle " + std::to_string(i) + " repeats stage " +
+                                          std::to_string(k));
         }
-        // Build first with borrowed pointers so a ChainMismatch leaves the
-        // caller's stage handles intact.
         for (int i = 0; i + 1 < n; ++i)
             if (!(stages[i]->p->output() == stages[i + 1]->p->input()) || !stages[i]->p->output().valid())
                 throw ChainMismatch("stage " + std::to_string(i) + " ('" + stages[i]->p->name() +
                                     "') output is not the input of stage " + std::to_string(i + 1) + " ('" +
                                     stages[i + 1]->p->name() + "')");
+        auto h = std::make_unique<hetreco_process_t>();
+        std::vector<std::unique_ptr<Process>> v;
         for (int i = 0; i < n; ++i) v.push_back(std::move(stages[i]->owned));
-        auto* h = new hetreco_process_t;
-        auto comp = chain(S(s), name ? name : "chain", std::move(v));
-        for (int i = 0; i < n; ++i) {
-            stages[i]->p = &comp->stage(i);  // caller's handles become views
+        std::unique_ptr<CompositeProcess> comp;
+        try {
+            comp = chain(S(s), name ? name : "chain", std::move(v));
+        } catch (...) {
+            // chain() leaves the stages in `v` when it throws: hand them back
+            for (int i = 0; i < n && i < int(v.size()); ++i)
+                if (v[i]) stages[i]->owned = std::move(v[i]);
+            throw;
         }
+        for (int i = 0; i < n; ++i) stages[i]->p = &comp->stage(i);  // caller's handles become views
         h->p = comp.get();
         h->owned = std::move(comp);
         for (int i = 0; i < n; ++i) h->stage_views.push_back(stages[i]);
-        *out = h;
+        *out = h.release();
     });
 }
 

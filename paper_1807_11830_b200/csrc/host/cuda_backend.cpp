@@ -52,6 +52,12 @@ int cuda_device_count() {
 
 // ---- CudaBackend ------------------------------------------------------------------------
 
+// Construction only reads the device properties (no context): the backend
+// list holds one CudaBackend per visible GPU, and a process that uses one GPU
+// (one rank per GPU under torchrun) must not open contexts, streams and
+// pinned rings on the others.  The device state is created on first use
+// (ensure()), like the reference's lazily populated backend list
+// (backend.cpp:294-313) but per device.
 CudaBackend::CudaBackend(int ordinal, std::uint64_t capacity) : ordinal_(ordinal), capacity_(capacity) {
     id_ = "cuda" + std::to_string(ordinal);
     cudaDeviceProp p{};
@@ -65,25 +71,32 @@ CudaBackend::CudaBackend(int ordinal, std::uint64_t capacity) : ordinal_(ordinal
     desc_.global_memory_bytes = capacity ? capacity : std::uint64_t(p.totalGlobalMem);
     desc_.base_alignment_bytes = 256;
     desc_.supports_source_kernels = nvrtc::available();
-    make_current();
+}
+
+void CudaBackend::ensure() const {
+    if (ready_.load(std::memory_order_acquire)) return;
+    std::lock_guard lk(init_mu_);
+    if (ready_.load(std::memory_order_relaxed)) return;
+    auto* self = const_cast<CudaBackend*>(this);
+    ck(cudaSetDevice(ordinal_), "cudaSetDevice");
     cudaMemPool_t pool = nullptr;
-    if (cudaDeviceGetDefaultMemPool(&pool, ordinal) == cudaSuccess) {
+    if (cudaDeviceGetDefaultMemPool(&pool, ordinal_) == cudaSuccess) {
         std::uint64_t keep = ~std::uint64_t(0);
         cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
     } else {
         cudaGetLastError();
     }
-    ck(cudaStreamCreateWithFlags(&compute_, cudaStreamNonBlocking), "cudaStreamCreate");
-    ck(cudaStreamCreateWithFlags(&h2d_, cudaStreamNonBlocking), "cudaStreamCreate");
-    ck(cudaStreamCreateWithFlags(&d2h_, cudaStreamNonBlocking), "cudaStreamCreate");
-    ck(cudaEventCreateWithFlags(&ev_compute_, cudaEventDisableTiming), "cudaEventCreate");
-    ck(cudaEventCreateWithFlags(&ev_copy_, cudaEventDisableTiming), "cudaEventCreate");
-    ring_size_ = 1u << 20;
-    ck(cudaHostAlloc(reinterpret_cast<void**>(&ring_host_), ring_size_, cudaHostAllocDefault), "cudaHostAlloc");
-    ck(cudaMalloc(reinterpret_cast<void**>(&ring_dev_), ring_size_), "cudaMalloc");
+    ck(cudaStreamCreateWithFlags(&self->compute_, cudaStreamNonBlocking), "cudaStreamCreate");
+    ck(cudaStreamCreateWithFlags(&self->h2d_, cudaStreamNonBlocking), "cudaStreamCreate");
+    ck(cudaStreamCreateWithFlags(&self->d2h_, cudaStreamNonBlocking), "cudaStreamCreate");
+    self->ring_size_ = 1u << 20;
+    ck(cudaHostAlloc(reinterpret_cast<void**>(&self->ring_host_), ring_size_, cudaHostAllocDefault), "cudaHostAlloc");
+    ck(cudaMalloc(reinterpret_cast<void**>(&self->ring_dev_), ring_size_), "cudaMalloc");
+    ready_.store(true, std::memory_order_release);
 }
 
 CudaBackend::~CudaBackend() {
+    if (!ready_.load()) return;
     cudaSetDevice(ordinal_);
     cudaStreamSynchronize(compute_);
     for (auto& [id, b] : bufs_) cudaFreeAsync(b.ptr, compute_);
@@ -92,8 +105,6 @@ CudaBackend::~CudaBackend() {
     if (cudaDeviceGetDefaultMemPool(&pool, ordinal_) == cudaSuccess) cudaMemPoolTrimTo(pool, 0);
     cudaFree(ring_dev_);
     cudaFreeHost(ring_host_);
-    cudaEventDestroy(ev_compute_);
-    cudaEventDestroy(ev_copy_);
     cudaStreamDestroy(compute_);
     cudaStreamDestroy(h2d_);
     cudaStreamDestroy(d2h_);
@@ -101,7 +112,10 @@ CudaBackend::~CudaBackend() {
     stager_.reset();
 }
 
-void CudaBackend::make_current() const { ck(cudaSetDevice(ordinal_), "cudaSetDevice"); }
+void CudaBackend::make_current() const {
+    ensure();
+    ck(cudaSetDevice(ordinal_), "cudaSetDevice");
+}
 
 const CudaBackend::Buf& CudaBackend::lookup(BufferId id) const {
     auto it = bufs_.find(id);
@@ -128,6 +142,7 @@ BufferId CudaBackend::allocate(std::uint64_t bytes) {
     }
     // zero-filled like the reference's buffers (backend.cpp:137-141), in queue order
     ck(cudaMemsetAsync(p, 0, bytes ? bytes : 1, compute_), "cudaMemsetAsync");
+    note_work();
     const BufferId id = next_++;
     bufs_.emplace(id, Buf{p, bytes});
     used_ += bytes;
@@ -141,6 +156,7 @@ void CudaBackend::release(BufferId id) {
     make_current();
     // stream-ordered: in-flight work on the compute stream finishes first
     cudaFreeAsync(it->second.ptr, compute_);
+    note_work();
     used_ -= it->second.size;
     bufs_.erase(it);
 }
@@ -161,6 +177,7 @@ void CudaBackend::upload(BufferId id, std::uint64_t off, std::span<const std::by
     check_window("upload", off, bytes.size(), b.size);
     if (bytes.empty()) return;
     make_current();
+    note_work();
     if (bytes.size() >= kStageMin && !detail::HostStager::is_pinned(bytes.data())) {
         try {
             stager().upload(static_cast<char*>(b.ptr) + off, bytes.data(), bytes.size(), compute_);
@@ -182,6 +199,7 @@ void CudaBackend::download(BufferId id, std::uint64_t off, std::span<std::byte> 
     check_window("download", off, into.size(), b.size);
     if (into.empty()) return;
     make_current();
+    note_work();
     if (into.size() >= kStageMin && !detail::HostStager::is_pinned(into.data())) {
         try {
             stager().download(into.data(), static_cast<const char*>(b.ptr) + off, into.size(), compute_);
@@ -207,6 +225,7 @@ void CudaBackend::copy(BufferId src, std::uint64_t so, BufferId dst, std::uint64
         throw InvalidArgument("overlapping copy within buffer " + std::to_string(src));
     if (n == 0) return;
     make_current();
+    note_work();
     ck(cudaMemcpyAsync(static_cast<char*>(d.ptr) + doff, static_cast<const char*>(s.ptr) + so, n,
                        cudaMemcpyDeviceToDevice, compute_),
        "cudaMemcpyAsync(D2D)");
@@ -309,6 +328,7 @@ void CudaBackend::execute(const CompiledKernel& kernel, const KernelBinding& bin
     args.params = stage_params(bind.params);
     args.params_size = bind.params.size();
     last_kernel_ = kernel.name;
+    note_work();
     cudaError_t e;
     if (jit) {
         // grid-stride entry: enough CTAs to fill the GPU, never more than needed
@@ -331,6 +351,7 @@ void CudaBackend::synchronize() {
 }
 
 void CudaBackend::check(const char* what) const {
+    ensure();
     cudaError_t e = cudaGetLastError();
     if (e == cudaSuccess) e = cudaStreamQuery(compute_);
     if (e != cudaSuccess && e != cudaErrorNotReady) throw DeviceError(what, cudaGetErrorString(e));

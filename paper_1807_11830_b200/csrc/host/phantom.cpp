@@ -57,6 +57,7 @@ Phantom gen_phantom(ComputeSession& s, const PhantomSpec& spec, HostMemory memor
         a.coil_width = 0.4 * L;
         int sms = 148;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, cb.ordinal());
+        cb.note_work();
         const cudaError_t e = dev::launch_phantom(a, sms, cb.compute_stream());
         if (e != cudaSuccess) throw DeviceError("gen_phantom", cudaGetErrorString(e));
         // Y_i = F(S_i . M_true): the forward model process, unmasked

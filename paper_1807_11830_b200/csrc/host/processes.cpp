@@ -199,6 +199,7 @@ struct Process::Timing {
     bool chained[kRing]{};
     int head = 0, pending = 0;
     int last = -1;  // slot of the most recent launch (its stop event stays valid until resolved + reused)
+    std::uint64_t seq_after = ~std::uint64_t(0);  // backend work_seq() right after that launch
     // "launch_timing": 0 = every launch (default), 1 = every kSample-th launch
     // (totals extrapolated from the sampled mean), 2 = off
     int mode = 0;
@@ -286,8 +287,12 @@ void Process::launch() {
     if (t.pending == Timing::kRing) resolve_timings();
     const int slot = (t.head + t.pending) % Timing::kRing;
     cudaSetDevice(t.device);
-    // chain to the previous launch only while it is still queued/running
-    const bool chain = t.pending > 0 && t.last >= 0 && cudaEventQuery(t.stop[t.last]) == cudaErrorNotReady;
+    // chain to the previous launch only while it is still queued/running AND
+    // nothing else was enqueued on the compute stream since (other processes,
+    // kernels, copies): otherwise that work would be counted as this launch's
+    CudaBackend& cb = session_.cuda();
+    const bool chain = t.pending > 0 && t.last >= 0 && cb.work_seq() == t.seq_after &&
+                       cudaEventQuery(t.stop[t.last]) == cudaErrorNotReady;
     if (!chain) {
         cudaGetLastError();  // a completed query is not an error
         cudaEventRecord(t.start[slot], t.stream);
@@ -295,6 +300,7 @@ void Process::launch() {
     t.chained[slot] = chain;
     on_launch();
     cudaEventRecord(t.stop[slot], t.stream);
+    t.seq_after = cb.work_seq();
     t.last = slot;
     t.pending += 1;
     stats_.launches += 1;
@@ -381,6 +387,7 @@ void GraphProcess::capture() {
     if (graph_) cudaGraphDestroy(graph_);
     graph_ = g;
     exec_ = x;
+    cb.note_work();
     ck(cudaGraphUpload(exec_, cb.compute_stream()), "cudaGraphUpload");
 }
 
@@ -397,6 +404,7 @@ std::vector<double> GraphProcess::profile(int reps) {
     CudaBackend& cb = session().cuda();
     cb.make_current();
     cudaStream_t s = cb.compute_stream();
+    cb.note_work();
     std::vector<double> acc;
     profiling_ = true;
     try {
@@ -427,6 +435,7 @@ std::vector<double> GraphProcess::profile(int reps) {
 
 void GraphProcess::on_launch() {
     CudaBackend& cb = session().cuda();
+    cb.note_work();
     const cudaError_t e = cudaGraphLaunch(exec_, cb.compute_stream());
     if (e != cudaSuccess) {
         cudaGetLastError();
@@ -436,23 +445,29 @@ void GraphProcess::on_launch() {
 
 // ---- CompositeProcess -------------------------------------------------------------------------
 
-CompositeProcess::CompositeProcess(ComputeSession& s, std::string name, std::vector<std::unique_ptr<Process>> stages)
-    : GraphProcess(s, std::move(name)), stages_(std::move(stages)) {
-    if (stages_.empty()) throw InvalidArgument("chain '" + this->name() + "' has no stages");
-    for (std::size_t i = 0; i < stages_.size(); ++i) {
-        if (!stages_[i]) throw InvalidArgument("chain stage " + std::to_string(i) + " is null");
-        if (&stages_[i]->session() != &s)
+// The stages are validated in the caller's vector and only taken over once
+// nothing can fail any more: a throwing constructor leaves them with the caller.
+CompositeProcess::CompositeProcess(ComputeSession& s, std::string name, std::vector<std::unique_ptr<Process>>&& stages)
+    : GraphProcess(s, std::move(name)) {
+    if (stages.empty()) throw InvalidArgument("chain '" + this->name() + "' has no stages");
+    for (std::size_t i = 0; i < stages.size(); ++i) {
+        if (!stages[i]) throw InvalidArgument("chain stage " + std::to_string(i) + " is null");
+        if (&stages[i]->session() != &s)
             throw ChainMismatch("stage " + std::to_string(i) + " belongs to another session");
-        if (!dynamic_cast<GraphProcess*>(stages_[i].get())) all_graph_ = false;
+        for (std::size_t k = 0; k < i; ++k)
+            if (stages[k].get() == stages[i].get())
+                throw InvalidArgument("chain stage " + std::to_string(i) + " repeats stage " + std::to_string(k));
+        if (!dynamic_cast<GraphProcess*>(stages[i].get())) all_graph_ = false;
     }
-    for (std::size_t i = 0; i + 1 < stages_.size(); ++i) {
-        if (!(stages_[i]->output() == stages_[i + 1]->input()) || !stages_[i]->output().valid())
-            throw ChainMismatch("stage " + std::to_string(i) + " ('" + stages_[i]->name() +
+    for (std::size_t i = 0; i + 1 < stages.size(); ++i) {
+        if (!(stages[i]->output() == stages[i + 1]->input()) || !stages[i]->output().valid())
+            throw ChainMismatch("stage " + std::to_string(i) + " ('" + stages[i]->name() +
                                 "') output is not the input of stage " + std::to_string(i + 1) + " ('" +
-                                stages_[i + 1]->name() + "')");
+                                stages[i + 1]->name() + "')");
     }
-    if (stages_.front()->input().valid()) set_input(stages_.front()->input());
-    if (stages_.back()->output().valid()) set_output(stages_.back()->output());
+    if (stages.front()->input().valid()) set_input(stages.front()->input());
+    if (stages.back()->output().valid()) set_output(stages.back()->output());
+    stages_ = std::move(stages);
 }
 
 void CompositeProcess::bake(const ProcessParams& params) {
@@ -492,7 +507,7 @@ void CompositeProcess::on_launch() {
     }
 }
 
-std::unique_ptr<CompositeProcess> chain(ComputeSession& s, std::string name, std::vector<std::unique_ptr<Process>> stages) {
+std::unique_ptr<CompositeProcess> chain(ComputeSession& s, std::string name, std::vector<std::unique_ptr<Process>>&& stages) {
     return std::make_unique<CompositeProcess>(s, std::move(name), std::move(stages));
 }
 
@@ -1203,6 +1218,7 @@ void StreamingRecon::run(const void* host_in, std::uint64_t frames, void* host_o
     CudaBackend& cb = m.session->cuda();
     cb.make_current();
     cudaStream_t cs = cb.compute_stream(), hs = cb.h2d_stream(), ds = cb.d2h_stream();
+    cb.note_work();
     const int sms = sm_count(cb.ordinal());
     const auto* src = static_cast<const char*>(host_in);
     auto* dst = static_cast<char*>(host_out);

@@ -29,6 +29,23 @@ __device__ __forceinline__ unsigned group_mask(int tid) {
     }
 }
 
+// Synchronises the T threads of coil group g.  Groups of <= 32 threads sit in
+// one warp (__syncwarp with the group's lane mask); wider groups (T = 64/128/256
+// at N = 1024/2048/4096) span several warps, so they use named barrier 1 + g
+// with a T-thread count (barrier 0 is __syncthreads), or the CTA barrier when
+// the CTA is a single group.
+template <int T, int G>
+__device__ __forceinline__ void group_sync(unsigned mask, int g) {
+    if constexpr (T <= 32) {
+        __syncwarp(mask);
+    } else if constexpr (G == 1) {
+        __syncthreads();
+    } else {
+        static_assert(T % 32 == 0 && G < 16, "named barriers need whole warps and ids < 16");
+        asm volatile("bar.sync %0, %1;" ::"r"(1 + g), "n"(T) : "memory");
+    }
+}
+
 template <int N>
 constexpr int cp_groups() {  // coil groups per CTA: ~128 threads
     constexpr int T = LineFFT<N>::T;
@@ -84,7 +101,7 @@ __global__ void __launch_bounds__(G * LineFFT<N>::T, cp_min_blocks<N, MODE>()) k
                 slots_ld<R>(sh_out, (long long)(R / 2) * T, [&](auto m, long long d) { sv[m.value] = __ldg(sp + T * m.value + d); });
             };
             if constexpr (SENSE && kEarlyMap) load_map();
-            L::template run<+1>(v, tw, line, j, [mask] { __syncwarp(mask); }, a.scale);
+            L::template run<+1>(v, tw, line, j, [mask, g] { group_sync<T, G>(mask, g); }, a.scale);
             if constexpr (SENSE && !kEarlyMap) load_map();
             if constexpr (SENSE) {
                 sfor<R>([&](auto m) { mac_conj(acc_re[m.value], acc_im[m.value], v[m.value], sv[m.value]); });

@@ -728,3 +728,86 @@ def test_large_pageable_transfers_through_staging_ring(s):
     assert beq(s.fetch_data(hp).arrays[0], b)
     s.release_data(hd)
     s.release_data(hp)
+
+
+@pytest.mark.parametrize("nx,ny,nc,nf", [(1024, 64, 8, 1), (2048, 32, 3, 1), (4096, 16, 2, 1), (1024, 96, 5, 2)])
+def test_coil_parallel_combine_wide_lines(s, monkeypatch, nx, ny, nc, nf):
+    """Coil-parallel combine with lines wider than a warp (T = 64/128/256
+    threads per coil group at N = 1024/2048/4096): the group exchange needs a
+    named barrier (or the CTA barrier), not __syncwarp."""
+    rng = np.random.default_rng(nx + ny + nc)
+    Y = cplx(rng, nx, ny, nc, nf)
+    S = cplx(rng, nx, ny, nc)
+    X = np.fft.ifft2(Y.astype(np.complex128), axes=(0, 1))
+    ref = (np.conj(S.astype(np.complex128))[..., None] * X).sum(axis=2)
+    rss = np.sqrt((np.abs(X) ** 2).sum(axis=2))
+    for forced in ("1", ""):
+        monkeypatch.setenv("HETRECO_COMBINE_CP", forced)
+        for _ in range(3):  # a race shows up as run-to-run differences too
+            (M,), _ = run_process(s, "sens_recon", [Y, S], [((nx, ny, nf), np.complex64)])
+            assert relmax(M, ref) <= TOL
+            (R,), _ = run_process(s, "rss_recon", [Y], [((nx, ny, nf), np.float32)])
+            assert relmax(R, rss) <= TOL
+
+
+def test_launch_stats_exclude_interleaved_work(s):
+    """LaunchStats chain a launch to the same process' previous stop event only
+    when nothing else was queued on the compute stream in between; a cheap
+    process interleaved with an expensive one must not absorb its time
+    (ADVICE r1, medium)."""
+    rng = np.random.default_rng(5)
+    x = np.asfortranarray(rng.random((64, 64), dtype=np.float32))
+    hx = s.register_data([x])
+    hy = s.allocate_data([((64, 64), np.float32)])
+    small = h.Process(s, "negate").set_input(hx).set_output(hy).init({"max_value": 1.0, "launch_timing": "every"})
+    Y = cplx(rng, 256, 256, 16, 8)
+    S = cplx(rng, 256, 256, 16)
+    hk = s.register_data(h.Data([Y, S], h.DataKind.KData))
+    hm = s.allocate_data([((256, 256, 8), np.complex64)], h.DataKind.XData)
+    big = h.Process(s, "sens_recon").set_input(hk).set_output(hm).init({"launch_timing": "every"})
+    s.synchronize()
+    for _ in range(30):
+        small.launch()
+        big.launch()
+    sm, bg = small.stats(), big.stats()
+    assert sm.launches == 30 and bg.launches == 30
+    assert sm.mean_launch_seconds() < 0.5 * bg.mean_launch_seconds(), (sm.mean_launch_seconds(), bg.mean_launch_seconds())
+    # back-to-back launches of one process still chain (and stay positive)
+    for _ in range(20):
+        big.launch()
+    bg2 = big.stats()
+    assert bg2.launches == 50 and bg2.last_launch_seconds > 0
+    for hd in (hx, hy, hk, hm):
+        s.release_data(hd)
+
+
+def test_chain_failure_leaves_stages_usable(s):
+    """hetreco_chain_create validates everything before taking ownership: a
+    repeated handle or a foreign-session stage fails and the caller's stage
+    handles keep working."""
+    rng = np.random.default_rng(9)
+    x = np.asfortranarray(rng.random((32, 32), dtype=np.float32))
+    ha = s.register_data([x])
+    hb = s.allocate_data([((32, 32), np.float32)])
+    p1 = h.Process(s, "negate").set_input(ha).set_output(hb)
+    p2 = h.Process(s, "negate").set_input(hb).set_output(hb)
+    with pytest.raises(h.HetrecoError):
+        h.chain(s, "dup", [p1, p1])
+    s2 = h.ComputeSession("gpu")
+    try:
+        y2 = s2.register_data([x])
+        q = h.Process(s2, "negate").set_input(y2).set_output(y2)
+        with pytest.raises(h.HetrecoError):
+            h.chain(s, "foreign", [p1, q])
+        q.init({"max_value": 1.0}).launch()
+        assert beq(s2.fetch_data(y2).arrays[0], o.negate(x, 1.0))
+        del q
+    finally:
+        s2.close()
+    with pytest.raises(h.HetrecoError):
+        h.chain(s, "empty", [])
+    p1.init({"max_value": 1.0}).launch()
+    assert beq(s.fetch_data(hb).arrays[0], o.negate(x, 1.0))
+    c = h.chain(s, "ok", [p1, p2])  # still chainable after the failures
+    c.init().launch()
+    assert beq(s.fetch_data(hb).arrays[0], o.negate(o.negate(x, 1.0), 1.0))
