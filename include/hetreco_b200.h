@@ -218,6 +218,22 @@ int hetreco_stream_create(hetreco_session s, int method, uint64_t nx, uint64_t n
 int hetreco_stream_run(hetreco_stream st, const void* host_kspace, uint64_t frames, void* host_out);
 int hetreco_stream_destroy(hetreco_stream st);
 
+/* ---- layer 2: one host volume over several GPUs by frame slab (SURVEY §8 e) ----
+ * No reference counterpart: the reference binds one device per session and has
+ * no multi-device path.  Slab g of G = frames
+ * [floor(g F / G), floor((g+1) F / G)); one worker thread + ComputeSession +
+ * streaming pipeline per entry of backend_ids (ids may repeat); no collective. */
+typedef struct hetreco_multi_t* hetreco_multi;
+int hetreco_frame_slab(uint64_t index, uint64_t count, uint64_t frames, uint64_t* begin, uint64_t* end);
+int hetreco_multi_create(int n, const char* const* backend_ids, int method, uint64_t nx, uint64_t ny, uint64_t coils,
+                         uint64_t chunk_frames, const void* host_smaps, int shift, int bind_numa, hetreco_multi* out);
+/* host_kspace [nx,ny,coils,frames] c64 -> host_out [nx,ny,frames]; blocks */
+int hetreco_multi_run(hetreco_multi m, const void* host_kspace, uint64_t frames, void* host_out);
+/* slab `index` of the last run: first frame, frame count, host seconds */
+int hetreco_multi_slab(hetreco_multi m, int index, uint64_t* first, uint64_t* frames, double* seconds);
+int hetreco_multi_device_count(hetreco_multi m, int* n);
+int hetreco_multi_destroy(hetreco_multi m);
+
 /* ---- host-only helpers (layout.hpp:37-65): pack + header wire format ----------- */
 /* pack(Data, alignment) then serialize_layout_header: writes (1+11*count) u64
  * words to `words` (cap in words) and offsets into arrays[i].offset_bytes. */

@@ -11,6 +11,7 @@
 
 #include "../kernels/launch.hpp"
 #include "hetreco_b200/io.hpp"
+#include "hetreco_b200/multi_gpu.hpp"
 #include "hetreco_b200/numa.hpp"
 #include "hetreco_b200/phantom.hpp"
 #include "nvrtc_compiler.hpp"
@@ -39,6 +40,9 @@ struct hetreco_process_t {
 };
 struct hetreco_stream_t {
     std::unique_ptr<StreamingRecon> r;
+};
+struct hetreco_multi_t {
+    std::unique_ptr<MultiGpuRecon> m;
 };
 struct hetreco_cuda_backend_t {
     std::unique_ptr<CudaBackend> b;
@@ -655,6 +659,65 @@ int hetreco_stream_run(hetreco_stream st, const void* in, uint64_t frames, void*
 
 int hetreco_stream_destroy(hetreco_stream st) {
     return guard([&] { delete st; });
+}
+
+int hetreco_frame_slab(uint64_t index, uint64_t count, uint64_t frames, uint64_t* begin, uint64_t* end) {
+    return guard([&] {
+        const auto [b, e] = frame_slab(index, count, frames);
+        if (begin) *begin = b;
+        if (end) *end = e;
+    });
+}
+
+int hetreco_multi_create(int n, const char* const* ids, int method, uint64_t nx, uint64_t ny, uint64_t coils,
+                         uint64_t chunk, const void* smaps, int shift, int bind_numa, hetreco_multi* out) {
+    return guard([&] {
+        need(out, "out");
+        if (n <= 0) throw InvalidArgument("multi-GPU recon needs at least one backend id");
+        need(ids, "backend_ids");
+        std::vector<std::string> v;
+        for (int i = 0; i < n; ++i) {
+            need(ids[i], "backend id");
+            v.emplace_back(ids[i]);
+        }
+        auto h = std::make_unique<hetreco_multi_t>();
+        h->m = std::make_unique<MultiGpuRecon>(
+            v, method == HETRECO_METHOD_SENSE ? StreamingRecon::Method::Sense : StreamingRecon::Method::Rss, nx, ny,
+            coils, chunk, smaps, shift != 0, bind_numa != 0);
+        *out = h.release();
+    });
+}
+
+int hetreco_multi_run(hetreco_multi m, const void* in, uint64_t frames, void* out) {
+    return guard([&] {
+        need(m, "multi");
+        m->m->run(in, frames, out);
+    });
+}
+
+int hetreco_multi_slab(hetreco_multi m, int index, uint64_t* first, uint64_t* frames, double* seconds) {
+    return guard([&] {
+        need(m, "multi");
+        const auto& r = m->m->last_run();
+        if (index < 0 || std::size_t(index) >= r.size())
+            throw InvalidArgument("slab " + std::to_string(index) + " out of range (last run had " +
+                                  std::to_string(r.size()) + ")");
+        if (first) *first = r[index].first_frame;
+        if (frames) *frames = r[index].frames;
+        if (seconds) *seconds = r[index].seconds;
+    });
+}
+
+int hetreco_multi_device_count(hetreco_multi m, int* n) {
+    return guard([&] {
+        need(m, "multi");
+        need(n, "n");
+        *n = int(m->m->device_count());
+    });
+}
+
+int hetreco_multi_destroy(hetreco_multi m) {
+    return guard([&] { delete m; });
 }
 
 // ---- host-only layout helpers ----

@@ -90,6 +90,8 @@ EXPORTED = [
     "hetreco_gen_phantom", "hetreco_phantom_blobs", "hetreco_nvrtc_compile_check", "hetreco_nvrtc_available",
     "hetreco_cuda_supports_source", "hetreco_cuda_compile", "hetreco_cuda_execute_unit",
     "hetreco_device_numa_node", "hetreco_bind_numa_node", "hetreco_parse_cpulist",
+    "hetreco_frame_slab", "hetreco_multi_create", "hetreco_multi_run", "hetreco_multi_slab",
+    "hetreco_multi_device_count", "hetreco_multi_destroy",
 ]
 
 
@@ -156,6 +158,10 @@ def lib():
         "hetreco_cuda_execute_unit": ([vp, pc, pc, u64, u64, u64, u64, vp, u64, u64], i32),
         "hetreco_device_numa_node": ([i32, vp], i32), "hetreco_bind_numa_node": ([i32, vp], i32),
         "hetreco_parse_cpulist": ([pc, vp, i32, vp], i32),
+        "hetreco_frame_slab": ([u64, u64, u64, vp, vp], i32),
+        "hetreco_multi_create": ([i32, vp, i32, u64, u64, u64, u64, vp, i32, i32, vp], i32),
+        "hetreco_multi_run": ([vp, vp, u64, vp], i32), "hetreco_multi_slab": ([vp, i32, vp, vp, vp], i32),
+        "hetreco_multi_device_count": ([vp, vp], i32), "hetreco_multi_destroy": ([vp], i32),
     })
     lenient = os.environ.get("HETRECO_LIB_LENIENT") == "1"  # A/B runs against older builds
     for name, (args, res) in sig.items():
@@ -711,6 +717,58 @@ class StreamingRecon:
         try:
             if self._h:
                 lib().hetreco_stream_destroy(self._h)
+        except Exception:
+            pass
+
+
+def frame_slab(index: int, count: int, frames: int) -> tuple[int, int]:
+    """[begin, end) frames of slab `index` of `count` (the library's partition)."""
+    b, e = C.c_uint64(), C.c_uint64()
+    _ck(lib().hetreco_frame_slab(index, count, frames, C.byref(b), C.byref(e)))
+    return b.value, e.value
+
+
+class MultiGpuRecon:
+    """One host k-space volume reconstructed over several GPUs by frame slab
+    (hetreco_multi_*): one worker thread, session and streaming pipeline per
+    backend id, each moving its own contiguous slab; no collective."""
+
+    def __init__(self, backend_ids: Sequence[str], method: str, nx: int, ny: int, coils: int, chunk_frames: int,
+                 smaps: np.ndarray | None = None, shift: bool = False, bind_numa: bool = True):
+        self.method = method
+        self.nx, self.ny, self.coils = nx, ny, coils
+        self.backend_ids = list(backend_ids)
+        smp = None if smaps is None else np.asfortranarray(smaps, dtype=np.complex64)
+        ids = (C.c_char_p * max(1, len(self.backend_ids)))(*[b.encode() for b in self.backend_ids])
+        self._h = C.c_void_p()
+        m = 0 if method == "sense" else 1
+        _ck(lib().hetreco_multi_create(len(self.backend_ids), ids, m, nx, ny, coils, chunk_frames,
+                                       smp.ctypes.data if smp is not None else None, int(shift), int(bind_numa),
+                                       C.byref(self._h)))
+
+    def run(self, kspace: np.ndarray, out: np.ndarray):
+        assert kspace.flags.f_contiguous and out.flags.f_contiguous
+        frames = kspace.size // (self.nx * self.ny * self.coils)
+        _ck(lib().hetreco_multi_run(self._h, kspace.ctypes.data, frames, out.ctypes.data))
+        return out
+
+    def slabs(self) -> list[dict]:
+        """Per slab of the last run: backend id, first frame, frames, seconds."""
+        res = []
+        for i, bid in enumerate(self.backend_ids):
+            f, n, t = C.c_uint64(), C.c_uint64(), C.c_double()
+            _ck(lib().hetreco_multi_slab(self._h, i, C.byref(f), C.byref(n), C.byref(t)))
+            res.append({"backend_id": bid, "first_frame": f.value, "frames": n.value, "seconds": t.value})
+        return res
+
+    def close(self):
+        if self._h:
+            _ck(lib().hetreco_multi_destroy(self._h))
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
         except Exception:
             pass
 
