@@ -1,19 +1,23 @@
 #!/usr/bin/env python
 """Benchmark: cardiac-cine SENSE reconstruction (BASELINE.json configs[2], C3).
 
-One step = one launch of the fused sens_recon process over one 256x256 x 32-coil
-x 30-frame cine (k-space + sensitivity maps resident in HBM; 496 MiB of input
-per step, larger than the 126 MB L2, so no flush is needed).  Per GPU the
-work is fixed (weak scaling): rank r reconstructs its own 30-frame slab.
+One step = reconstruct one 256x256 x 32-coil x 30-frame cine end to end:
+k-space from pinned host memory -> H2D -> fused IFFT2 + conj-sensitivity coil
+combine -> D2H -> images in pinned host memory, through the public streaming
+API (hetreco_stream_run).  Under torchrun the 30 frames are split into
+contiguous frame slabs over the ranks (strong scaling, no collective on the
+data path); rank r streams only its slab.
 
     python bench.py [--gpus N --steps K --warmup W] [--impl reference]
 
-Prints ONE JSON line (rank 0).  `value` = frames/s over all ranks with data
-resident (device time, CUDA events on the processes' compute stream, max over
-ranks); `e2e` = the same metric through the public streaming API from pinned
-host memory with H2D+D2H inside the timed region; `roofline` = the dominant
-kernel against MEASURED_PEAKS.json; `cpu_baseline` = the reference library
-(oracle/_ref, its own ComputeSession API) on this host's cores.
+Prints ONE JSON line (rank 0).  `value` = `e2e.value` = frames/s of the whole
+volume (device time between CUDA events on each rank's compute stream, which
+the pipeline joins after its last D2H; max over ranks).  Side fields:
+`device_resident` (the same chain with the slab already in HBM), `roofline`
+(the dominant kernel against MEASURED_PEAKS.json), `weak_scaling` (N > 1:
+every rank a whole volume), `cpu_baseline` (the reference library,
+oracle/_ref, through its own ComputeSession API on this host's cores) and
+`other_configs` (C1, C2, C4 resident; C5 streamed and sharded like C3).
 """
 from __future__ import annotations
 
@@ -34,14 +38,20 @@ sys.path.insert(0, ROOT)
 NX, NY, NC, NF = 256, 256, 32, 30
 METRIC = "recon frames/s end-to-end incl. H2D/D2H at 1/2/4/8 GPU; kernel HBM GB/s vs peak"
 UNIT = "frames/s"
-CONFIG = {"workload": "C3 cardiac cine SENSE: 256x256 k-space, 32 coils x 30 frames per GPU, "
-                      "IFFT2 + conj-sensitivity coil combine",
-          "nx": NX, "ny": NY, "coils": NC, "frames_per_gpu": NF, "dtype_io": "complex64",
+CONFIG = {"workload": "C3 cardiac cine SENSE: 256x256 k-space, 32 coils x 30 frames (one volume; "
+                      "frames sharded over the GPUs), IFFT2 + conj-sensitivity coil combine",
+          "nx": NX, "ny": NY, "coils": NC, "frames": NF, "dtype_io": "complex64",
           "l2_policy": "inputs (496 MiB/step) larger than L2 (126 MB); no flush"}
 # algorithmic bytes (SURVEY.md §8 d): Y 16 MiB + M 0.5 MiB per frame, S 16 MiB once per launch
 FRAME_Y = NX * NY * NC * 8
 FRAME_M = NX * NY * 8
 SMAP = NX * NY * NC * 8
+C5_NX, C5_NC = 512, 32
+
+
+def config_for(world: int) -> dict:
+    """The config dict both arms print (identical keys and values)."""
+    return dict(CONFIG, parallelism=f"frame-slab x{world} (no collective)")
 
 
 def peaks():
@@ -53,37 +63,43 @@ def peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks/throttle reasons sampled while the GPU is loaded."""
+    """nvidia-smi clocks/throttle reasons sampled while the timed regions run."""
 
+    REASONS = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap", "gpu_idle"]
     Q = ("index,clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-         "clocks_event_reasons.sw_power_cap")
+         "clocks_event_reasons.sw_power_cap,clocks_event_reasons.gpu_idle")
 
     def __init__(self, gpu_index: int):
         self.idx = gpu_index
         self.rows = []
         self._stop = threading.Event()
-        self._t = None
+        self._on = threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
 
     def _run(self):
         while not self._stop.is_set():
-            try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.Q}",
-                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
-                                     timeout=5).stdout.strip()
-                if out:
-                    self.rows.append([x.strip() for x in out.split(",")])
-            except Exception:
-                pass
-            self._stop.wait(0.05)
+            if self._on.wait(0.05) and not self._stop.is_set():
+                try:
+                    out = subprocess.run(["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                         timeout=5).stdout.strip()
+                    if out and self._on.is_set():
+                        self.rows.append([x.strip() for x in out.split(",")])
+                except Exception:
+                    pass
+                self._stop.wait(0.05)
 
-    def __enter__(self):
-        self._t = threading.Thread(target=self._run, daemon=True)
-        self._t.start()
-        return self
+    def on(self):
+        self._on.set()
 
-    def __exit__(self, *a):
+    def off(self):
+        self._on.clear()
+
+    def close(self):
         self._stop.set()
+        self._on.set()
         self._t.join()
 
     def summary(self):
@@ -91,13 +107,13 @@ class ClockSampler:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"], "samples": 0}
         sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
         mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 4 + i and r[4 + i] == "Active"})
+        reasons = sorted({n for r in self.rows for i, n in enumerate(self.REASONS)
+                          if len(r) > 4 + i and r[4 + i] == "Active"})
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
                 "reasons": reasons, "samples": len(self.rows)}
 
 
-def dist_setup(n_gpus: int):
+def dist_setup():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -128,75 +144,84 @@ def barrier(world: int):
         dist.barrier()
 
 
-def make_inputs(seed: int):
-    rng = np.random.default_rng(seed)
-    Y = np.empty((NX, NY, NC, NF), np.complex64, order="F")
-    for f in range(NF):  # chunked to bound temporaries
-        re = rng.standard_normal((NX, NY, NC), dtype=np.float32)
-        im = rng.standard_normal((NX, NY, NC), dtype=np.float32)
-        Y[..., f] = re + 1j * im
+def fill_frames(Y, first: int):
+    """Y[..., i] = C3 frame first + i (seeded per frame, so every rank makes
+    exactly its own slab of the same volume)."""
+    for i in range(Y.shape[3]):
+        rng = np.random.default_rng([1234, first + i])
+        Y[..., i] = (rng.standard_normal((NX, NY, NC), dtype=np.float32)
+                     + 1j * rng.standard_normal((NX, NY, NC), dtype=np.float32))
+    return Y
+
+
+def make_maps():
+    rng = np.random.default_rng(99)
     G = (rng.standard_normal((NX, NY, NC), dtype=np.float32) + 1j * rng.standard_normal((NX, NY, NC), dtype=np.float32))
-    S = np.asfortranarray((G / np.sqrt((np.abs(G) ** 2).sum(axis=2, keepdims=True))).astype(np.complex64))
-    return Y, S
+    return np.asfortranarray((G / np.sqrt((np.abs(G) ** 2).sum(axis=2, keepdims=True))).astype(np.complex64))
 
 
-def cpu_baseline(Y, S, budget_s: float = 12.0):
-    """The reference library itself (oracle/_ref) on a bounded sample."""
+def make_inputs():
+    """The whole C3 volume in pageable memory (reference arm / CPU baseline)."""
+    Y = fill_frames(np.empty((NX, NY, NC, NF), np.complex64, order="F"), 0)
+    return Y, make_maps()
+
+
+def cpu_baseline(Y, S, budget_s: float = 10.0):
+    """The reference library itself (oracle/_ref) on all 30 C3 frames per launch."""
     from oracle import oracle as o
-    sample = 2
-    Ys = np.asfortranarray(Y[..., :sample])
     if o.reference_available():
         kind = "reference"
-        _, t1, _ = o.ref_recon("sens", Ys, S, reps=1)  # warm-up + estimate
+        _, t1, _ = o.ref_recon("sens", Y, S, reps=1)  # warm-up + estimate
         reps = max(2, min(50, int(budget_s / max(t1, 1e-3))))
-        _, mean_s, _ = o.ref_recon("sens", Ys, S, reps=reps)
+        _, mean_s, _ = o.ref_recon("sens", Y, S, reps=reps)
         cores = o.ref_pool_threads()
     else:  # reference not built on this host: single-thread C port
         kind = "port"
         t0 = time.perf_counter()
-        o.sens_recon(Ys, S)
+        o.sens_recon(Y, S)
         mean_s = time.perf_counter() - t0
         reps, cores = 1, 1
-    return {"value": sample / mean_s, "unit": UNIT, "cores": cores, "kind": kind,
-            "sample": f"{sample} of the 30 C3 frames (256x256x32 coils) per launch, {reps} launches, "
-                      f"plan baked once; WorkerPool threads = min(hw, 16), host has {os.cpu_count()} cores",
-            "seconds_per_frame": mean_s / sample}
+    return {"value": NF / mean_s, "unit": UNIT, "cores": cores, "kind": kind,
+            "sample": f"all 30 C3 frames (256x256x32 coils) per launch, {reps} launches, plan baked once; "
+                      f"WorkerPool threads = min(hw, 16), host has {os.cpu_count()} cores",
+            "seconds_per_frame": mean_s / NF}
 
 
 def run_reference(args):
     """The reference's own CPU implementation (oracle/_ref: the unmodified
-    reference library driven through its ComputeSession API).  One step =
-    register the k-space of a bounded frame sample (the reference's H2D),
-    run the SENSE chain, fetch the images (D2H); sensitivity maps and the FFT
-    plan are set up once, as on the B200 arm."""
+    reference library driven through its ComputeSession API) on the same
+    workload as our arm.  One step = register the k-space of all 30 frames (the
+    reference's H2D), run the SENSE chain (fft_radix2_pass x18 +
+    complex_element_prod + ximage_sum), fetch the images (D2H); sensitivity
+    maps and the FFT plan are set up once, as on the B200 arm.  Under torchrun
+    rank 0 alone runs it (one CPU implementation per host)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     from oracle import oracle as o
-    Y, S = make_inputs(1234)
-    sample = 2
-    Ys = np.asfortranarray(Y[..., :sample])
+    Y, S = make_inputs()
     if o.reference_available():
         kind = "reference"
-        o.ref_recon_e2e("sens", Ys, S, reps=max(1, min(args.warmup, 2)))
-        _, mean_s = o.ref_recon_e2e("sens", Ys, S, reps=args.steps)
+        o.ref_recon_e2e("sens", Y, S, reps=max(1, min(args.warmup, 2)))
+        _, mean_s = o.ref_recon_e2e("sens", Y, S, reps=args.steps)
         cores = o.ref_pool_threads()
     else:
         kind = "port"
-        o.sens_recon(Ys, S)
+        o.sens_recon(Y, S)
         t0 = time.perf_counter()
         for _ in range(args.steps):
-            o.sens_recon(Ys, S)
+            o.sens_recon(Y, S)
         mean_s = (time.perf_counter() - t0) / args.steps
         cores = 1
-    value = sample / mean_s
+    value = NF / mean_s
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": mean_s * 1e3, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded N(0,1) k-space)",
-            "config": dict(CONFIG, sample_frames_per_step=sample), "impl": "reference",
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32 (complex64 I/O, fp32 FFT, fp64 coil accumulation)",
+            "data": "synthetic (seeded N(0,1) k-space, normalised random sensitivity maps)",
+            "config": config_for(int(os.environ.get("WORLD_SIZE", "1"))), "impl": "reference",
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind,
-                             "sample": f"{sample} of 30 C3 frames per step: register_data(k-space) + "
-                                       f"fft_radix2_pass x18 + complex_element_prod + ximage_sum + fetch_data; "
+                             "sample": "all 30 C3 frames per step: register_data(k-space) + fft_radix2_pass x18 + "
+                                       "complex_element_prod + ximage_sum + fetch_data; "
                                        f"WorkerPool threads = min(hw,16) of {os.cpu_count()} host cores"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -204,53 +229,95 @@ def run_reference(args):
 
 def run_ours(args):
     from paper_1807_11830_b200 import hetreco as h
+    from paper_1807_11830_b200.sharding import frame_slab, imbalance
 
-    rank, world, local = dist_setup(args.gpus)
+    rank, world, local = dist_setup()
     # host placement: this rank's thread and pinned buffers on its GPU's NUMA node
     # (the CPU-baseline leg below gets the whole host back)
     all_cpus = os.sched_getaffinity(0)
     numa_node = h.bind_to_device_numa(local)
-    devs = h.enumerate_devices()
+    devs = h.enumerate_devices()  # descriptors only: no context on the other GPUs
     s = h.ComputeSession(device=devs[local])
-    Y, S = make_inputs(1234 + rank)
-    hin = s.register_data(h.Data([Y, S], h.DataKind.KData))
-    hout = s.allocate_data([((NX, NY, NF), np.complex64)], h.DataKind.XData)
-    p = h.Process(s, "sens_recon").set_input(hin).set_output(hout).init()
-
+    # strong scaling: one 30-frame volume, rank r owns frames [b, e)
+    fb, fe = frame_slab(rank, world, NF)
+    nfr = fe - fb
+    S = make_maps()
+    Yp = fill_frames(h.pinned_empty((NX, NY, NC, nfr), np.complex64), fb)
+    Mp = h.pinned_empty((NX, NY, nfr), np.complex64)
+    chunk = max(1, min(args.chunk, (nfr + 1) // 2))
+    st = h.StreamingRecon(s, "sense", NX, NY, NC, chunk, S)
+    chunks_per_run = (nfr + chunk - 1) // chunk
     sampler = ClockSampler(local)
-    with sampler:
-        # warm-up: W steps, extended to >= 0.5 s of load so clocks settle
-        t_end = time.perf_counter() + 0.5
-        n = 0
-        while n < args.warmup or time.perf_counter() < t_end:
-            p.launch()
-            n += 1
-            if n % 50 == 0:
-                s.synchronize()
-        s.synchronize()
-        barrier(world)
-        s.synchronize()
-        s.timer_start()
-        for _ in range(args.steps):
-            p.launch()
-        t_dev = s.timer_stop()  # synchronizes the compute stream
-        barrier(world)
-    t_max = reduce_max(t_dev, world)
-    value = NF * world * args.steps / t_max
-    clocks = sampler.summary()
+
+    # ---- headline: end to end through the public streaming API -----------------------
+    # pinned k-space slab -> H2D (copy stream) -> fused IFFT2 + SENSE -> D2H
+    # (second copy stream) -> pinned image slab, every step inside the timed
+    # region; device time between CUDA events on the session's compute stream
+    # (the pipeline joins it after the last D2H), max over ranks.
+    sampler.on()
+    t_end = time.perf_counter() + 0.5
+    n = 0
+    while n < args.warmup or time.perf_counter() < t_end:
+        st.run(Yp, Mp)
+        n += 1
+    barrier(world)
+    w0 = time.perf_counter()
+    s.timer_start()
+    for _ in range(args.steps):
+        st.run(Yp, Mp)
+    t_e2e = s.timer_stop()
+    wall_e2e = time.perf_counter() - w0
+    barrier(world)
+    sampler.off()
+    t_e2e_max = reduce_max(t_e2e, world)
+    wall_e2e_max = reduce_max(wall_e2e, world)
+    value = NF * args.steps / t_e2e_max
+    e2e = {"value": value, "unit": UNIT, "h2d_bytes_per_step": FRAME_Y * NF, "d2h_bytes_per_step": FRAME_M * NF,
+           "h2d_bytes_per_step_per_rank": FRAME_Y * nfr, "chunk_frames": chunk,
+           "wall_value": NF * args.steps / wall_e2e_max,
+           "host_link_gbs_per_rank": FRAME_Y * nfr * args.steps / t_e2e / 1e9,
+           "note": "hetreco_stream_run over this rank's pinned frame slab; sensitivity maps uploaded once at "
+                   "init (resident), k-space H2D and images D2H per step"}
+
+    # ---- device-resident side measurement (same slab, data already in HBM) -----------
+    hin = s.register_data(h.Data([np.asfortranarray(Yp), S], h.DataKind.KData))
+    hout = s.allocate_data([((NX, NY, nfr), np.complex64)], h.DataKind.XData)
+    p = h.Process(s, "sens_recon").set_input(hin).set_output(hout).init()
+    sampler.on()
+    t_end = time.perf_counter() + 0.5
+    n = 0
+    while n < args.warmup or time.perf_counter() < t_end:
+        p.launch()
+        n += 1
+        if n % 50 == 0:
+            s.synchronize()
+    s.synchronize()
+    barrier(world)
+    s.timer_start()
+    dev_steps = max(args.steps, 50)
+    for _ in range(dev_steps):
+        p.launch()
+    t_dev = s.timer_stop()
+    barrier(world)
+    sampler.off()
+    t_dev_max = reduce_max(t_dev, world)
+    M_dev = s.fetch_data(hout).arrays[0]
+    e2e["matches_resident"] = bool(np.abs(M_dev - Mp).max() <= 1e-5 * np.abs(M_dev).max())
+    device_resident = {"value": NF * dev_steps / t_dev_max, "unit": UNIT, "steps": dev_steps,
+                       "ms_per_step": t_dev_max / dev_steps * 1e3,
+                       "note": "sens_recon process over the rank's slab resident in HBM (no host transfers)"}
 
     # per-kernel device times (events between kernels on the compute stream)
     prof = p.profile(reps=10)  # [axis1, combine] per frame chunk (one chunk by default)
     k_axis1, k_axis0 = sum(prof[0::2]), sum(prof[1::2])
-    bytes_axis1 = 2 * FRAME_Y * NF                 # read Y, write X
-    bytes_axis0 = FRAME_Y * NF + SMAP + FRAME_M * NF  # read X + S, write M
+    bytes_axis1 = 2 * FRAME_Y * nfr                 # read Y, write X
+    bytes_axis0 = FRAME_Y * nfr + SMAP + FRAME_M * nfr  # read X + S, write M
     peak, peak_kind = peaks()
     kernels = [
-        {"name": "k_fft_strided_ring<256,+1,16,2,32> (axis-1 IFFT, 32-column tiles through a 2-stage cp.async shared-memory ring)", "seconds": k_axis1, "bytes": bytes_axis1,
-         "gbs": bytes_axis1 / k_axis1 / 1e9},
+        {"name": "k_fft_strided_ring<256,+1,16,2,32> (axis-1 IFFT, 32-column tiles through a 2-stage cp.async "
+                 "shared-memory ring)", "seconds": k_axis1, "bytes": bytes_axis1, "gbs": bytes_axis1 / k_axis1 / 1e9},
         {"name": "k_fft_combine_ss<256,4> (axis-0 IFFT + conj(S) coil combine, map rows staged in smem)",
-         "seconds": k_axis0,
-         "bytes": bytes_axis0, "gbs": bytes_axis0 / k_axis0 / 1e9},
+         "seconds": k_axis0, "bytes": bytes_axis0, "gbs": bytes_axis0 / k_axis0 / 1e9},
     ]
     for k in kernels:
         k["frac"] = k["gbs"] / peak
@@ -258,58 +325,58 @@ def run_ours(args):
     dom = max(kernels, key=lambda k: k["seconds"])
     traffic = None
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(tp):
+    if os.path.exists(tp) and nfr == NF:
         tj = json.load(open(tp))
         traffic = tj.get("per_launch_bytes", {}).get("axis1" if dom is kernels[0] else "axis0")
-    algo_step = NF * (FRAME_Y + FRAME_M) + SMAP
+    algo_step = nfr * (FRAME_Y + FRAME_M) + SMAP
     roofline = {"bound": "hbm", "achieved": dom["gbs"], "peak": peak, "unit": "GB/s", "frac": dom["frac"],
                 "traffic": traffic, "peak_source": peak_kind, "kernel": dom["name"],
-                "kernels": kernels,
-                "chain_achieved": algo_step / (t_max / args.steps) / 1e9,
-                "chain_frac": algo_step / (t_max / args.steps) / 1e9 / peak,
+                "kernels": kernels, "frames_per_launch": nfr,
+                "chain_achieved": algo_step / (t_dev / dev_steps) / 1e9,
+                "chain_frac": algo_step / (t_dev / dev_steps) / 1e9 / peak,
                 "algorithmic_bytes_per_step": algo_step}
 
-    # end-to-end through the public streaming API (pinned host memory)
-    e2e = None
-    if not args.no_e2e:
-        Yp = h.pinned_empty((NX, NY, NC, NF), np.complex64)
-        Yp[...] = Y
-        Mp = h.pinned_empty((NX, NY, NF), np.complex64)
-        st = h.StreamingRecon(s, "sense", NX, NY, NC, args.chunk, S)
-        for _ in range(max(1, args.warmup // 4)):
-            st.run(Yp, Mp)
+    # host-link roofline: plain pinned H2D copy of the same bytes on this GPU
+    link = h.CudaBackend(local)
+    buf = link.allocate(Yp.nbytes)
+    flat = Yp.reshape(-1, order="F").view(np.uint8)
+    link.upload(buf, 0, flat)
+    t0 = time.perf_counter()
+    for _ in range(3):
+        link.upload(buf, 0, flat)
+    link_gbs = 3 * Yp.nbytes / (time.perf_counter() - t0) / 1e9
+    link.release(buf)
+    link.close()
+    e2e["host_link_peak_gbs_per_rank"] = link_gbs
+    e2e["host_link_frac"] = e2e["host_link_gbs_per_rank"] / link_gbs
+    e2e["host_link_roofline_frames_per_s"] = world * link_gbs * 1e9 / FRAME_Y
+    s.release_data(hin)
+    s.release_data(hout)
+
+    # weak scaling side field: every rank streams a whole 30-frame volume
+    weak = None
+    if world > 1 and not args.no_weak:
+        Yw = fill_frames(h.pinned_empty((NX, NY, NC, NF), np.complex64), 0)
+        Mw = h.pinned_empty((NX, NY, NF), np.complex64)
+        stw = h.StreamingRecon(s, "sense", NX, NY, NC, args.chunk, S)
+        stw.run(Yw, Mw)
         barrier(world)
-        t0 = time.perf_counter()
-        e2e_steps = max(3, min(args.steps, 20))
-        for _ in range(e2e_steps):
-            st.run(Yp, Mp)
-        t_e2e = time.perf_counter() - t0
-        barrier(world)
-        t_e2e = reduce_max(t_e2e, world)
-        e2e = {"value": NF * world * e2e_steps / t_e2e, "unit": UNIT, "h2d_bytes_per_step": FRAME_Y * NF,
-               "d2h_bytes_per_step": FRAME_M * NF, "steps": e2e_steps, "chunk_frames": args.chunk,
-               "host_link_gbs": FRAME_Y * NF * e2e_steps / t_e2e / 1e9,
-               "note": "sensitivity maps uploaded once at init (resident), k-space streamed per step"}
-        # streamed result equals the resident process output
-        M_dev = s.fetch_data(hout).arrays[0]
-        e2e["matches_resident"] = bool(np.abs(M_dev - Mp).max() <= 1e-5 * np.abs(M_dev).max())
-        # host-link roofline: plain pinned H2D copy of the same bytes on this box
-        link = h.CudaBackend(local)
-        buf = link.allocate(Yp.nbytes)
-        link.upload(buf, 0, Yp.reshape(-1, order="F").view(np.uint8))
-        t0 = time.perf_counter()
-        for _ in range(3):
-            link.upload(buf, 0, Yp.reshape(-1, order="F").view(np.uint8))
-        link_gbs = 3 * Yp.nbytes / (time.perf_counter() - t0) / 1e9
-        link.release(buf)
-        link.close()
-        # the reference arm's flow through the operator API with plain
-        # (pageable) numpy buffers: register k-space, launch, fetch, release
-        # -- per step, as --impl reference does on the CPU
+        s.timer_start()
+        wsteps = max(3, min(args.steps, 20))
+        for _ in range(wsteps):
+            stw.run(Yw, Mw)
+        tw = reduce_max(s.timer_stop(), world)
+        weak = {"value": world * NF * wsteps / tw, "unit": UNIT, "frames_per_gpu": NF, "steps": wsteps}
+        del stw, Yw, Mw
+
+    # the reference-shaped flow (rank 0, N=1): register pageable k-space + maps,
+    # launch, fetch, release per step
+    if rank == 0 and world == 1 and not args.no_session_flow:
+        Y = np.asfortranarray(Yp)
+        hout = s.allocate_data([((NX, NY, NF), np.complex64)], h.DataKind.XData)
         hs = s.register_data(h.Data([Y], h.DataKind.KData))
         s.release_data(hs)
         Mh = np.empty((NX, NY, NF), np.complex64, order="F")
-        smap_h = s.register_data(h.Data([S], h.DataKind.Generic))
         ps = None
         t0 = time.perf_counter()
         for _ in range(5):
@@ -322,39 +389,101 @@ def run_ours(args):
             s.fetch_data(hout, [Mh])
             s.release_data(hk)
         t_sess = (time.perf_counter() - t0) / 5
-        s.release_data(smap_h)
+        s.release_data(hout)
         e2e["session_api_pageable"] = {
-            "value": NF * world / t_sess, "unit": UNIT, "ms_per_step": t_sess * 1e3,
+            "value": NF / t_sess, "unit": UNIT, "ms_per_step": t_sess * 1e3,
             "h2d_bytes_per_step": FRAME_Y * NF + SMAP, "d2h_bytes_per_step": FRAME_M * NF,
             "note": "register_data(pageable k-space + maps) + sens_recon launch + fetch_data per step "
                     "(the --impl reference flow); pinned staging ring on the host side"}
-        e2e["host_link_peak_gbs"] = link_gbs
-        e2e["host_link_frac"] = e2e["host_link_gbs"] / link_gbs
-        e2e["host_link_roofline_frames_per_s"] = NF * world * link_gbs * 1e9 / (FRAME_Y * NF)
+
+    # C5 (all ranks): 512^2 x 32 coils, args.c5_frames frames sharded over the
+    # ranks, streamed from pinned memory
+    c5 = None
+    if args.c5_frames > 0 and not args.no_extras:
+        c5 = c5_stream(h, s, rank, world, args.c5_frames, sampler)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         os.sched_setaffinity(0, all_cpus)
-        cpu = cpu_baseline(Y, S)
+        Yc, Sc = make_inputs()
+        cpu = cpu_baseline(Yc, Sc)
+        del Yc
 
     extras = None
     if rank == 0 and not args.no_extras:
-        extras = other_configs(h, s, peak, args.c5_frames)
+        extras = other_configs(h, s, peak)
+        if c5:
+            extras["C5_stream_rss_512x512x32"] = c5
+    sampler.close()
+    clocks = sampler.summary()
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-                "warmup": args.warmup, "ms_per_step": t_max / args.steps * 1e3, "higher_is_better": True,
-                "scaling": "weak", "vs_baseline": None, "dtype": "f32 (complex64 I/O, fp32 FFT and coil accumulation)",
+                "warmup": args.warmup, "ms_per_step": t_e2e_max / args.steps * 1e3, "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None,
+                "dtype": "f32 (complex64 I/O, fp32 FFT and coil accumulation)",
                 "data": "synthetic (seeded N(0,1) k-space, normalised random sensitivity maps)",
-                "config": dict(CONFIG, parallelism=f"frame-slab x{world} (no collective)",
-                               host_numa_node_rank0=numa_node),
+                "config": config_for(world),
+                "sharding": {"frames_per_gpu": [frame_slab(r, world, NF)[1] - frame_slab(r, world, NF)[0]
+                                                for r in range(world)],
+                             "slab_imbalance": imbalance(world, NF), "host_numa_node_rank0": numa_node},
                 "impl": "hetreco-b200",
-                "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu, "clocks": clocks,
-                "gpu_launches": 2 * args.steps, "other_configs": extras}
+                "e2e": e2e, "device_resident": device_resident, "weak_scaling": weak,
+                "roofline": roofline, "cpu_baseline": cpu, "clocks": clocks,
+                "gpu_launches": 2 * chunks_per_run * args.steps, "other_configs": extras}
         print(json.dumps(line), flush=True)
     if world > 1:
         import torch.distributed as dist
         dist.destroy_process_group()
+
+
+def c5_stream(h, s, rank: int, world: int, total_frames: int, sampler):
+    """C5: 512^2 x 32-coil k-space, `total_frames` frames split into contiguous
+    slabs over the ranks, each streamed from its rank's pinned buffer (RSS);
+    the streamed images are checked against the resident rss_recon process."""
+    from paper_1807_11830_b200.sharding import frame_slab
+    fb, fe = frame_slab(rank, world, total_frames)
+    nfr = fe - fb
+    n, nc = C5_NX, C5_NC
+    Y5 = h.pinned_empty((n, n, nc, nfr), np.complex64)
+    rng = np.random.default_rng(5)
+    base = (rng.standard_normal((n, n, nc), dtype=np.float32)
+            + 1j * rng.standard_normal((n, n, nc), dtype=np.float32)).astype(np.complex64)
+    for i in range(nfr):  # distinct frames at memcpy speed (16 GiB at N=1)
+        np.multiply(base, np.float32(1.0 + 0.01 * (fb + i)), out=Y5[..., i])
+    R5 = h.pinned_empty((n, n, nfr), np.float32)
+    st5 = h.StreamingRecon(s, "rss", n, n, nc, 2)
+    st5.run(Y5, R5)
+    barrier(world)
+    sampler.on()
+    s.timer_start()
+    reps = 2
+    for _ in range(reps):
+        st5.run(Y5, R5)
+    t5 = reduce_max(s.timer_stop(), world) / reps
+    sampler.off()
+    # parity: streamed frames (first chunk and the tail) == resident rss_recon
+    ok = True
+    for f0 in sorted({0, max(0, nfr - 2)}):
+        f1 = min(nfr, f0 + 2)
+        hk = s.register_data(h.Data([np.asfortranarray(Y5[..., f0:f1])], h.DataKind.KData))
+        hr = s.allocate_data([((n, n, f1 - f0), np.float32)], h.DataKind.XData)
+        pr = h.Process(s, "rss_recon").set_input(hk).set_output(hr).init()
+        pr.launch()
+        Rr = s.fetch_data(hr).arrays[0]
+        ok &= bool(np.abs(Rr - R5[..., f0:f1]).max() <= 1e-5 * max(np.abs(Rr).max(), 1e-30))
+        if f0 == 0:
+            td = _device_time(s, pr.launch, 20)
+            dev_fps = (f1 - f0) / td
+        s.release_data(hk)
+        s.release_data(hr)
+    ok = reduce_max(0.0 if ok else 1.0, world) == 0.0
+    del Y5, R5, st5
+    return {"frames_total": total_frames, "ranks": world, "frames_rank0": nfr, "frames_per_s": total_frames / t5,
+            "seconds_per_step": t5, "host_link_gbs_rank0": nfr * n * n * nc * 8 / t5 / 1e9,
+            "matches_resident": ok, "device_frames_per_s_rank0": dev_fps,
+            "device_gbs_rank0": dev_fps * (n * n * nc * 8 + n * n * 4) / 1e9,
+            "note": "pinned H2D of 64 MiB/frame (PCIe) dominates; slabs of one volume over the ranks"}
 
 
 def _device_time(s, fn, reps: int) -> float:
@@ -368,10 +497,9 @@ def _device_time(s, fn, reps: int) -> float:
     return s.timer_stop() / reps
 
 
-def other_configs(h, s, peak: float, c5_frames: int):
-    """Side measurements for BASELINE.json configs 0, 1, 3, 4 (the headline is
-    config 2 = C3).  All device-resident except C5, which streams from pinned
-    host memory like the e2e leg."""
+def other_configs(h, s, peak: float):
+    """Side measurements for BASELINE.json configs 0, 1, 3 (device resident; C5
+    is c5_stream, the headline is config 2 = C3)."""
     rng = np.random.default_rng(99)
     out = {}
     # C1: Negate on one 512x512 float32 image (paper's minimal example)
@@ -423,42 +551,21 @@ def other_configs(h, s, peak: float, c5_frames: int):
         "init_calls": st.init_calls, "init_ms": st.init_seconds * 1e3,
         "us_per_launch_device_sampled_stats": c4["sampled"][0] * 1e6,
         "kernels_per_launch": 3, "note": "one cudaGraphLaunch per launch(); plans/twiddles baked in init()"}
-    # C5: 512x512x32 coils streamed from pinned host memory (RSS), per GPU slab
-    if c5_frames > 0:
-        Y5 = h.pinned_empty((512, 512, 32, c5_frames), np.complex64)
-        for f in range(c5_frames):
-            Y5[..., f] = (rng.standard_normal((512, 512, 32), dtype=np.float32)
-                          + 1j * rng.standard_normal((512, 512, 32), dtype=np.float32))
-        R5 = h.pinned_empty((512, 512, c5_frames), np.float32)
-        st5 = h.StreamingRecon(s, "rss", 512, 512, 32, 2)
-        st5.run(Y5, R5)
-        t0 = time.perf_counter()
-        for _ in range(3):
-            st5.run(Y5, R5)
-        t5 = (time.perf_counter() - t0) / 3
-        out["C5_stream_rss_512x512x32"] = {"frames_per_gpu": c5_frames, "frames_per_s": c5_frames / t5,
-                                           "host_link_gbs": Y5.nbytes / t5 / 1e9,
-                                           "note": "pinned H2D of 64 MiB/frame dominates (PCIe)"}
-        hk5 = s.register_data(h.Data([np.asfortranarray(Y5[..., :2])], h.DataKind.KData))
-        hr5 = s.allocate_data([((512, 512, 2), np.float32)], h.DataKind.XData)
-        p5 = h.Process(s, "rss_recon").set_input(hk5).set_output(hr5).init()
-        t5d = _device_time(s, p5.launch, 20)
-        out["C5_stream_rss_512x512x32"]["device_frames_per_s"] = 2 / t5d
-        out["C5_stream_rss_512x512x32"]["device_gbs"] = 2 * (512 * 512 * 32 * 8 + 512 * 512 * 4) / t5d / 1e9
     return out
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
-    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--chunk", type=int, default=6, help="frames per streamed chunk (e2e)")
-    ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-session-flow", action="store_true")
+    ap.add_argument("--no-weak", action="store_true")
     ap.add_argument("--no-extras", action="store_true", help="skip the C1/C2/C4/C5 side measurements")
-    ap.add_argument("--c5-frames", type=int, default=8, help="frames of the C5 512^2x32 streamed slab")
+    ap.add_argument("--c5-frames", type=int, default=256, help="frames of the C5 512^2x32 volume (all ranks)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

@@ -1258,6 +1258,12 @@ void StreamingRecon::run(const void* host_in, std::uint64_t frames, void* host_o
            "D2H chunk");
         ck(cudaEventRecord(m.o_free[b], ds), "record o_free");
     }
+    // join: later work on the compute stream (and events recorded there, e.g.
+    // a device timer around run()) is ordered after the last D2H
+    if (frames) {
+        const int last_b = int(((frames + chunk_ - 1) / chunk_ - 1) & 1);
+        ck(cudaStreamWaitEvent(cs, m.o_free[last_b], 0), "join D2H");
+    }
     const cudaError_t e = cudaStreamSynchronize(ds);
     if (e != cudaSuccess) throw DeviceError("streaming_recon", cudaGetErrorString(e));
     ck(cudaStreamSynchronize(cs), "streaming recon (compute)");
