@@ -168,3 +168,45 @@ def test_sense_forward_oracle_vs_numpy():
     lhs = np.vdot(o.sense_forward(M, S, mask), y)
     rhs = np.vdot(M, o.sens_recon(np.asfortranarray(y.astype(np.complex64)), S)) * 32 * 32
     assert abs(lhs - rhs) <= 1e-4 * abs(lhs)
+
+
+# ---- BASELINE shapes: one C3 frame (256^2 x 32) and one C5 frame (512^2 x 32) ------------
+
+def _large_cases():
+    import json
+    import os
+    here = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+    return json.load(open(os.path.join(here, "large_shapes.json")))["cases"]
+
+
+def _large_inputs(case):
+    import os
+    import sys
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden"))
+    import synth
+    nx, ny, nc, nf, seed = case["nx"], case["ny"], case["coils"], case["frames"], case["seed"]
+    return synth.cplx(seed, nx, ny, nc, nf), synth.cplx(seed + 1, nx, ny, nc)
+
+
+@pytest.mark.parametrize("case", _large_cases(), ids=lambda c: c["name"])
+def test_port_matches_reference_golden_at_baseline_shapes(case):
+    """The C port reproduces the reference's output bytes (SHA-256 from
+    tests/golden/make_golden_large.py, run against oracle/_ref) at the
+    headline shapes, not only at 32x16: radix-2 plan of
+    fft_radix2_pass.cl.src:22-69 over 256/512 points, conj-S sum of
+    ximage_sum.cl.src:6-23 / rss_combine.cl.src:5-20 over 32 coils."""
+    import hashlib
+    Y, S = _large_inputs(case)
+    out = o.sens_recon(Y, S) if case["method"] == "sens" else o.rss_recon(Y)
+    assert hashlib.sha256(out.tobytes(order="F")).hexdigest() == case["sha256"]
+
+
+@pytest.mark.skipif(not o.reference_available(), reason="oracle/_ref not built")
+@pytest.mark.parametrize("shape", [(256, 256, 32, 1), (512, 512, 32, 1)])
+def test_port_matches_reference_live_baseline_shapes(shape):
+    nx, ny, nc, nf = shape
+    rng = np.random.default_rng(nx + 7)
+    Y = cplx(rng, nx, ny, nc, nf)
+    S = cplx(rng, nx, ny, nc)
+    assert beq(o.sens_recon(Y, S), o.ref_recon("sens", Y, S)[0])
+    assert beq(o.rss_recon(Y), o.ref_recon("rss", Y)[0])
