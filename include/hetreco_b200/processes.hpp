@@ -58,8 +58,10 @@ private:
 };
 
 // process.hpp:55-64.  Launch times are device time between CUDA events
-// recorded around each launch on the compute stream; they are resolved when
-// stats() is read (which waits for the last launch).
+// recorded around timed launches on the compute stream; they are resolved when
+// stats() is read (which waits for the last launch).  Process::init param
+// "launch_timing": "sampled" (default: every 16th launch timed, totals
+// extrapolated from the sampled mean), "every" or "off".
 struct LaunchStats {
     std::uint64_t init_calls = 0;
     std::uint64_t launches = 0;
@@ -116,7 +118,7 @@ private:
     mutable LaunchStats stats_;
     struct Timing;
     std::unique_ptr<Timing> timing_;
-    int timing_mode_ = 0;  // "launch_timing": 0 every, 1 sampled, 2 off
+    int timing_mode_ = 1;  // "launch_timing": 0 every, 1 sampled (default), 2 off
 };
 
 // A process whose device work is recorded once into a CUDA graph.

@@ -200,9 +200,9 @@ struct Process::Timing {
     int head = 0, pending = 0;
     int last = -1;  // slot of the most recent launch (its stop event stays valid until resolved + reused)
     std::uint64_t seq_after = ~std::uint64_t(0);  // backend work_seq() right after that launch
-    // "launch_timing": 0 = every launch (default), 1 = every kSample-th launch
+    // "launch_timing": 0 = every launch, 1 = every kSample-th launch (default)
     // (totals extrapolated from the sampled mean), 2 = off
-    int mode = 0;
+    int mode = 1;
     static constexpr std::uint64_t kSample = 16;
     double sampled_seconds = 0.0;
     std::uint64_t sampled = 0;
@@ -247,7 +247,9 @@ void Process::init(const ProcessParams& params) {
     const auto t0 = std::chrono::steady_clock::now();
     // generic key: "launch_timing" = "every" | "sampled" | "off" (LaunchStats cost:
     // a timed CUDA event record is ~3 us of host time per launch on B200)
-    const std::string lt = params.get_string("launch_timing", "every");
+    // default "sampled": a timed launch costs two event records of host time,
+    // which doubles the launch cost of a small process in a tight loop (C1, C4)
+    const std::string lt = params.get_string("launch_timing", "sampled");
     if (lt != "every" && lt != "sampled" && lt != "off")
         throw InvalidParams("launch_timing must be \"every\", \"sampled\" or \"off\"");
     timing_mode_ = lt == "every" ? 0 : lt == "sampled" ? 1 : 2;
@@ -358,6 +360,51 @@ void GraphProcess::on_rebind() {
     capture();
 }
 
+namespace {
+
+// Programmatic dependent launch inside process graphs (HETRECO_PDL=1, opt-in):
+// every kernel -> kernel edge of a captured graph becomes a programmatic edge
+// (kernels/pdl.cuh: the upstream kernel triggers at entry, the downstream one
+// waits before it touches data), so the launch of kernel i+1 and its prologue
+// overlap the tail of kernel i.  Measured on B200 (profiles/round2_small_
+// configs.md): no gain on the small configs (C2 8.47 -> 8.46 us, C4 12.75 ->
+// 12.56 us) and C3 slower (266 -> 329 us), so full-completion edges stay the
+// default.
+bool pdl_enabled() {
+    static const bool on = [] {
+        const char* v = std::getenv("HETRECO_PDL");
+        return v && *v == '1';
+    }();
+    return on;
+}
+
+void make_kernel_edges_programmatic(cudaGraph_t g) {
+    if (!pdl_enabled()) return;
+    size_t n = 0;
+    if (cudaGraphGetEdges_v2(g, nullptr, nullptr, nullptr, &n) != cudaSuccess || n == 0) {
+        cudaGetLastError();
+        return;
+    }
+    std::vector<cudaGraphNode_t> from(n), to(n);
+    std::vector<cudaGraphEdgeData> data(n);
+    ck(cudaGraphGetEdges_v2(g, from.data(), to.data(), data.data(), &n), "cudaGraphGetEdges");
+    for (size_t i = 0; i < n; ++i) {
+        cudaGraphNodeType a{}, b{};
+        ck(cudaGraphNodeGetType(from[i], &a), "cudaGraphNodeGetType");
+        ck(cudaGraphNodeGetType(to[i], &b), "cudaGraphNodeGetType");
+        if (a != cudaGraphNodeTypeKernel || b != cudaGraphNodeTypeKernel) continue;
+        if (data[i].type == cudaGraphDependencyTypeProgrammatic) continue;
+        ck(cudaGraphRemoveDependencies_v2(g, &from[i], &to[i], &data[i], 1), "cudaGraphRemoveDependencies");
+        cudaGraphEdgeData e{};
+        e.from_port = cudaGraphKernelNodePortProgrammatic;
+        e.to_port = 0;
+        e.type = cudaGraphDependencyTypeProgrammatic;
+        ck(cudaGraphAddDependencies_v2(g, &from[i], &to[i], &e, 1), "cudaGraphAddDependencies(programmatic)");
+    }
+}
+
+}  // namespace
+
 void GraphProcess::capture() {
     CudaBackend& cb = session().cuda();
     cb.make_current();
@@ -377,6 +424,12 @@ void GraphProcess::capture() {
     const cudaError_t e = cudaStreamEndCapture(cs, &g);
     cudaStreamDestroy(cs);
     ck(e, "capture of process '" + name() + "'");
+    try {
+        make_kernel_edges_programmatic(g);
+    } catch (...) {
+        cudaGraphDestroy(g);
+        throw;
+    }
     cudaGraphExec_t x = nullptr;
     const cudaError_t ei = cudaGraphInstantiate(&x, g, 0);
     if (ei != cudaSuccess) {

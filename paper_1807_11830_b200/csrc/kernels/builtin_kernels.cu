@@ -12,6 +12,7 @@
 #include <cstring>
 
 #include "launch.hpp"
+#include "pdl.cuh"
 
 namespace hetreco::dev {
 
@@ -41,6 +42,8 @@ __device__ __forceinline__ float2 cmul_rn(float2 a, float2 b) {
 
 // negate.cl.src:6-22
 __global__ void k_negate(hetreco_kernel_args a, std::uint64_t n) {
+    pdl_launch_dependents();
+    pdl_wait();
     const double mv = param<double>(a, 0);
     const std::uint64_t type = hetreco_hdr_type(a.in_layout, 0);
     if (type == HETRECO_UINT8) {
@@ -62,6 +65,8 @@ __global__ void k_negate(hetreco_kernel_args a, std::uint64_t n) {
 
 // fft_radix2_pass.cl.src:22-69
 __global__ void k_fft_radix2_pass(hetreco_kernel_args a, std::uint64_t n) {
+    pdl_launch_dependents();
+    pdl_wait();
     const std::uint32_t mode = param<std::uint32_t>(a, 0);
     const std::uint64_t L = param<std::uint64_t>(a, 8);
     const std::uint64_t S = param<std::uint64_t>(a, 16);
@@ -108,6 +113,8 @@ __global__ void k_fft_radix2_pass(hetreco_kernel_args a, std::uint64_t n) {
 
 // complex_element_prod.cl.src:9-19
 __global__ void k_complex_element_prod(hetreco_kernel_args a, std::uint64_t n) {
+    pdl_launch_dependents();
+    pdl_wait();
     const std::uint32_t conj = param<std::uint32_t>(a, 0);
     const float2* x = static_cast<const float2*>(arr_in(a, 0));
     const float2* s = static_cast<const float2*>(arr_in(a, 1));
@@ -122,6 +129,8 @@ __global__ void k_complex_element_prod(hetreco_kernel_args a, std::uint64_t n) {
 
 // ximage_sum.cl.src:6-23
 __global__ void k_ximage_sum(hetreco_kernel_args a, std::uint64_t n) {
+    pdl_launch_dependents();
+    pdl_wait();
     const std::uint64_t plane = hetreco_hdr_dim(a.in_layout, 0, 0) * hetreco_hdr_dim(a.in_layout, 0, 1);
     const std::uint64_t nc = hetreco_hdr_dim(a.in_layout, 0, 2);
     const float2* in = static_cast<const float2*>(arr_in(a, 0));
@@ -140,6 +149,8 @@ __global__ void k_ximage_sum(hetreco_kernel_args a, std::uint64_t n) {
 
 // rss_combine.cl.src:5-20
 __global__ void k_rss_combine(hetreco_kernel_args a, std::uint64_t n) {
+    pdl_launch_dependents();
+    pdl_wait();
     const std::uint64_t plane = hetreco_hdr_dim(a.in_layout, 0, 0) * hetreco_hdr_dim(a.in_layout, 0, 1);
     const std::uint64_t nc = hetreco_hdr_dim(a.in_layout, 0, 2);
     const float2* in = static_cast<const float2*>(arr_in(a, 0));
@@ -158,6 +169,8 @@ __global__ void k_rss_combine(hetreco_kernel_args a, std::uint64_t n) {
 
 // matrix_add.cl.src:5-24
 __global__ void k_matrix_add(hetreco_kernel_args a, std::uint64_t n) {
+    pdl_launch_dependents();
+    pdl_wait();
     const std::uint64_t type = hetreco_hdr_type(a.in_layout, 0);
     if (type == HETRECO_FLOAT32) {
         const float* x = static_cast<const float*>(arr_in(a, 0));
@@ -188,6 +201,8 @@ __device__ __forceinline__ unsigned char neg_u8(unsigned char x, double mv) {
 
 __global__ void k_negate_f32_vec(const float4* __restrict__ in, float4* __restrict__ out, std::uint64_t n4,
                                  const float* __restrict__ tin, float* __restrict__ tout, int tail, float m) {
+    pdl_launch_dependents();
+    pdl_wait();
     GRID_STRIDE(g, n4) {
         const float4 v = __ldcs(in + g);
         __stcs(out + g, make_float4(__fsub_rn(m, v.x), __fsub_rn(m, v.y), __fsub_rn(m, v.z), __fsub_rn(m, v.w)));
@@ -198,6 +213,8 @@ __global__ void k_negate_f32_vec(const float4* __restrict__ in, float4* __restri
 __global__ void k_negate_u8_vec(const uint4* __restrict__ in, uint4* __restrict__ out, std::uint64_t n16,
                                 const unsigned char* __restrict__ tin, unsigned char* __restrict__ tout, int tail,
                                 double mv) {
+    pdl_launch_dependents();
+    pdl_wait();
     // u8 results depend only on the byte value: build the 256-entry table once
     // per block with the reference's double formula (bit-exact), then map.
     __shared__ unsigned char lut[256];

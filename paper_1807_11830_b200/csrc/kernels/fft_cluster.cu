@@ -132,6 +132,8 @@ struct ClusterArgs {
 template <int MODE, int kCL>
 __global__ void __launch_bounds__(Geo<kCL>::threads, Geo<kCL>::min_blocks)
     k_recon_cluster(const __grid_constant__ CUtensorMap ymap, ClusterArgs a) {
+    pdl_launch_dependents();
+    pdl_wait();
     using L = CL256;
     using G = Geo<kCL>;
     constexpr int kTX = G::TX, kRY = G::RY, kThreads = G::threads, kLS = G::LS, kBuf = G::buf;

@@ -63,6 +63,7 @@ constexpr int cp_min_blocks() {
 
 template <int N, int MODE, int G>
 __global__ void __launch_bounds__(G * LineFFT<N>::T, cp_min_blocks<N, MODE>()) k_fft_combine_cp(ContigArgs a, std::uint32_t items) {
+    pdl_launch_dependents();
     using L = LineFFT<N>;
     constexpr int R = L::R, T = L::T;
     constexpr bool SENSE = MODE == int(Combine::Sense);
@@ -73,6 +74,7 @@ __global__ void __launch_bounds__(G * LineFFT<N>::T, cp_min_blocks<N, MODE>()) k
     const unsigned mask = group_mask<T>(tid);
     typename L::Twiddles tw;
     L::load_twiddles(tw, a.tw, j, a.scale);
+    pdl_wait();  // twiddle tables are init-time constants
     const bool sh_in = a.shift_in, sh_out = a.shift_out;
     const std::uint32_t C = std::uint32_t(a.coils), ny = std::uint32_t(a.ny);
     const IndexSplit ysplit(ny);

@@ -31,6 +31,7 @@ int ss_lines(std::uint64_t N) {
 template <int N, int LPB>
 __global__ void __launch_bounds__(LPB * LineFFT<N>::T) k_fft_combine_ss(ContigArgs a, std::uint32_t gpy,
                                                                         std::uint32_t groups) {
+    pdl_launch_dependents();
     using L = LineFFT<N>;
     constexpr int R = L::R, T = L::T, NT = LPB * T;
     constexpr int NS = (N + NT - 1) / NT;  // map elements staged per thread
@@ -41,6 +42,7 @@ __global__ void __launch_bounds__(LPB * LineFFT<N>::T) k_fft_combine_ss(ContigAr
     float2* line = smem + l * line_stride<N>();
     typename L::Twiddles tw;
     L::load_twiddles(tw, a.tw, j, a.scale);
+    pdl_wait();  // twiddle tables are init-time constants
     const bool sh_in = a.shift_in, sh_out = a.shift_out;
     const std::uint32_t C = std::uint32_t(a.coils), ny = std::uint32_t(a.ny), F = std::uint32_t(a.frames);
     const std::uint64_t coil_stride = std::uint64_t(ny) * N;

@@ -62,6 +62,7 @@ constexpr int tma_rows() {  // rows per CTA: a ~16 KB tile
 template <int N, int MODE, int LPB, int K>
 __global__ void __launch_bounds__(LPB * LineFFT<N>::T)
     k_fft_combine_tma(ContigArgs a, std::uint32_t groups_per_frame, std::uint32_t groups) {
+    pdl_launch_dependents();
     using L = LineFFT<N>;
     constexpr int R = L::R, T = L::T;
     constexpr bool SENSE = MODE == int(Combine::Sense);
@@ -75,6 +76,7 @@ __global__ void __launch_bounds__(LPB * LineFFT<N>::T)
     float2* line = xch + l * line_stride<N>();
     typename L::Twiddles tw;
     L::load_twiddles(tw, a.tw, j, a.scale);
+    pdl_wait();  // twiddle tables are init-time constants
     const bool sh_in = a.shift_in, sh_out = a.shift_out;
     const std::uint32_t C = std::uint32_t(a.coils), ny = std::uint32_t(a.ny);
     const std::uint64_t coil_elems = std::uint64_t(ny) * N;

@@ -25,6 +25,8 @@
 #include <type_traits>
 #include <utility>
 
+#include "pdl.cuh"
+
 namespace hetreco::dev {
 
 // ---- compile-time helpers ---------------------------------------------------------

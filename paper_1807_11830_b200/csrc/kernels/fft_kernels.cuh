@@ -62,6 +62,7 @@ constexpr int line_stride() {
 // MINB > 1 asks ptxas for MINB resident 256-thread CTAs per SM (register cap).
 template <int N, int DIR, int NXC, int RQ = default_points(N), bool PFS = false, int MINB = 1>
 __global__ void __launch_bounds__(MINB > 1 ? 256 : 512, MINB > 1 ? MINB : 0) k_fft_strided(StridedArgs a, int tx, std::uint32_t ntiles) {
+    pdl_launch_dependents();
     using L = LineFFT<N, RQ>;
     constexpr int R = L::R, T = L::T;
     extern __shared__ float2 smem[];
@@ -70,6 +71,7 @@ __global__ void __launch_bounds__(MINB > 1 ? 256 : 512, MINB > 1 ? MINB : 0) k_f
     float2* line = smem + l * line_stride<N>();
     typename L::Twiddles tw;
     L::load_twiddles(tw, a.tw, j, a.scale);
+    pdl_wait();  // twiddle tables are init-time constants
     const std::uint32_t nx = NXC ? std::uint32_t(NXC) : std::uint32_t(a.nx);
     const std::uint32_t xtiles = nx / std::uint32_t(tx);
     const IndexSplit xsplit(xtiles);
@@ -141,6 +143,7 @@ __device__ __forceinline__ void line_sync() {
 
 template <int N, int DIR>
 __global__ void __launch_bounds__(256) k_fft_contig(ContigArgs a, int lpb, std::uint32_t items) {
+    pdl_launch_dependents();
     using L = LineFFT<N>;
     constexpr int R = L::R, T = L::T;
     extern __shared__ float2 smem[];
@@ -149,6 +152,7 @@ __global__ void __launch_bounds__(256) k_fft_contig(ContigArgs a, int lpb, std::
     float2* line = smem + l * line_stride<N>();
     typename L::Twiddles tw;
     L::load_twiddles(tw, a.tw, j, a.scale);
+    pdl_wait();  // twiddle tables are init-time constants
     const bool sh_in = a.shift_in, sh_out = a.shift_out;
     for (std::uint32_t grp = blockIdx.x; grp * lpb < items; grp += gridDim.x) {
         const std::uint32_t item = grp * lpb + l;
@@ -176,6 +180,7 @@ __global__ void __launch_bounds__(256) k_fft_contig(ContigArgs a, int lpb, std::
 // iteration, 2 = ping-pong register buffers (loop unrolled by two).
 template <int N, int MODE, bool ACCF, int PF, int RQ = default_points(N), int MINB = 1>
 __global__ void __launch_bounds__(MINB > 1 ? 128 : 256, MINB > 1 ? MINB : 0) k_fft_combine(ContigArgs a, int lpb, std::uint32_t items) {
+    pdl_launch_dependents();
     using L = LineFFT<N, RQ>;
     constexpr int R = L::R, T = L::T;
     constexpr bool SENSE = MODE == int(Combine::Sense);
@@ -186,6 +191,7 @@ __global__ void __launch_bounds__(MINB > 1 ? 128 : 256, MINB > 1 ? MINB : 0) k_f
     float2* line = smem + l * line_stride<N>();
     typename L::Twiddles tw;
     L::load_twiddles(tw, a.tw, j, a.scale);
+    pdl_wait();  // twiddle tables are init-time constants
     const bool sh_in = a.shift_in, sh_out = a.shift_out;
     const std::uint32_t C = std::uint32_t(a.coils);
     const std::uint32_t ny = std::uint32_t(a.ny);

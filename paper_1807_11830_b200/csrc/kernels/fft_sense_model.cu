@@ -25,6 +25,7 @@ __device__ __forceinline__ float2 cmul_ref(float2 a, float2 b) {
 
 template <int N>
 __global__ void __launch_bounds__(256) k_fft_expand(ContigArgs a, int lpb, std::uint32_t items) {
+    pdl_launch_dependents();
     using L = LineFFT<N>;
     constexpr int R = L::R, T = L::T;
     extern __shared__ float2 smem[];
@@ -33,6 +34,7 @@ __global__ void __launch_bounds__(256) k_fft_expand(ContigArgs a, int lpb, std::
     float2* line = smem + l * line_stride<N>();
     typename L::Twiddles tw;
     L::load_twiddles(tw, a.tw, j, 1.0f);
+    pdl_wait();  // twiddle tables are init-time constants
     const bool sh_in = a.shift_in, sh_out = a.shift_out;
     const std::uint32_t ny = std::uint32_t(a.ny), C = std::uint32_t(a.coils);
     const IndexSplit ysplit(ny);
@@ -57,6 +59,7 @@ __global__ void __launch_bounds__(256) k_fft_expand(ContigArgs a, int lpb, std::
 
 template <int N, bool RT>
 __global__ void __launch_bounds__(256) k_fft_strided_masked(StridedArgs a, int tx, std::uint32_t ntiles) {
+    pdl_launch_dependents();
     using L = LineFFT<N>;
     constexpr int R = L::R, T = L::T;
     constexpr std::uint32_t NX = N;  // square images
@@ -66,6 +69,7 @@ __global__ void __launch_bounds__(256) k_fft_strided_masked(StridedArgs a, int t
     float2* line = smem + l * line_stride<N>();
     typename L::Twiddles tw;  // forward twiddles, scale 1
     L::load_twiddles(tw, a.tw, j, 1.0f);
+    pdl_wait();  // twiddle tables are init-time constants
     const std::uint32_t xtiles = NX / std::uint32_t(tx);
     const IndexSplit xsplit(xtiles);
     const bool sh_in = a.shift_in, sh_out = a.shift_out;

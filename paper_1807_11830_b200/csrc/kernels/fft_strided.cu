@@ -31,6 +31,7 @@ __device__ __forceinline__ void cp_async_wait() {
 
 template <int N, int DIR, int RQ, int K, int TX>
 __global__ void __launch_bounds__(TX * (N / RQ)) k_fft_strided_ring(StridedArgs a, std::uint32_t ntiles) {
+    pdl_launch_dependents();
     using L = LineFFT<N, RQ>;
     constexpr int R = L::R, T = L::T, NT = TX * T;
     constexpr int TILE = N * TX;        // float2 per stage
@@ -42,6 +43,7 @@ __global__ void __launch_bounds__(TX * (N / RQ)) k_fft_strided_ring(StridedArgs 
     float2* line = smem + K * TILE + l * line_stride<N>();
     typename L::Twiddles tw;
     L::load_twiddles(tw, a.tw, j, a.scale);
+    pdl_wait();  // twiddle tables are init-time constants
     constexpr std::uint32_t nx = N, xtiles = N / TX;
     constexpr std::uint64_t plane_elems = std::uint64_t(N) * N;
     const bool sh_in = a.shift_in, sh_out = a.shift_out;

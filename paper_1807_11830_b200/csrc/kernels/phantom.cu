@@ -6,12 +6,15 @@
 #include <cuda_runtime.h>
 
 #include "launch.hpp"
+#include "pdl.cuh"
 
 namespace hetreco::dev {
 
 namespace {
 
 __global__ void k_phantom(PhantomArgs a) {
+    pdl_launch_dependents();
+    pdl_wait();
     const std::uint64_t npix = std::uint64_t(a.nx) * a.ny;
     constexpr double kTwoPi = 6.283185307179586476925286766559;
     for (std::uint64_t p = blockIdx.x * std::uint64_t(blockDim.x) + threadIdx.x; p < npix;

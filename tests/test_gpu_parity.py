@@ -681,13 +681,14 @@ def test_recon_overlap_pipeline_bitexact(s, method):
 
 
 def test_launch_timing_modes(s):
-    """LaunchStats under "launch_timing": every launch timed (default), every
-    16th (totals extrapolated), or off; bad values rejected."""
+    """LaunchStats under "launch_timing": every launch timed, every 16th
+    (the default; totals extrapolated), or off; bad values rejected."""
     x = np.asfortranarray(np.random.default_rng(3).random((256, 256), dtype=np.float32))
     hx = s.register_data([x])
     hy = s.allocate_data([((256, 256), np.float32)])
-    for mode in ("every", "sampled", "off"):
-        p = h.Process(s, "negate").set_input(hx).set_output(hy).init({"max_value": 1.0, "launch_timing": mode})
+    for mode in ("every", "sampled", "off", None):
+        params = {"max_value": 1.0} if mode is None else {"max_value": 1.0, "launch_timing": mode}
+        p = h.Process(s, "negate").set_input(hx).set_output(hy).init(params)
         for _ in range(40):
             p.launch()
         st = p.stats()
