@@ -141,14 +141,22 @@ protected:
     virtual void bake(const ProcessParams& params) = 0;
     // Re-validate after a handle change (default: bake with the same params).
     virtual void rebake() { bake(params_); }
-    void capture();
+    // Re-read the device pointers after a handle change that kept every array
+    // shape and type (SPEC "re-point between launches"): plans, twiddles and
+    // scratch stay, the graph is re-recorded and patched in place with
+    // cudaGraphExecUpdate instead of re-instantiated.  Default: rebake().
+    virtual void repoint() { rebake(); }
+    // update: try cudaGraphExecUpdate of the existing executable first.
+    void capture(bool update = false);
     // Processes call mark(s) after each kernel they enqueue in record().
     void mark(cudaStream_t s);
     // true while profile() replays record() kernel by kernel (no graph)
     bool profiling() const { return profiling_; }
 
 private:
+    void snapshot_layouts();
     ProcessParams params_;
+    LayoutDescriptor in_snap_, out_snap_;  // layouts the current plans were baked for
     bool profiling_ = false;
     std::vector<cudaEvent_t> marks_;
     cudaGraph_t graph_ = nullptr;
@@ -166,6 +174,7 @@ public:
 protected:
     void bake(const ProcessParams& params) override;
     void rebake() override {}
+    void repoint() override {}
     void on_launch() override;
 
 private:

@@ -347,17 +347,29 @@ GraphProcess::~GraphProcess() {
     if (graph_) cudaGraphDestroy(graph_);
 }
 
+void GraphProcess::snapshot_layouts() {
+    in_snap_ = input().valid() ? session().layout_of(input()) : LayoutDescriptor{};
+    out_snap_ = output().valid() ? session().layout_of(output()) : LayoutDescriptor{};
+}
+
 void GraphProcess::on_init(const ProcessParams& params) {
     params_ = params;
     session().cuda().make_current();
     bake(params);
     capture();
+    snapshot_layouts();
 }
 
 void GraphProcess::on_rebind() {
     session().cuda().make_current();
-    rebake();
-    capture();
+    const bool same = (!input().valid() || session().layout_of(input()) == in_snap_) &&
+                      (!output().valid() || session().layout_of(output()) == out_snap_);
+    if (same)
+        repoint();
+    else
+        rebake();
+    capture(same);
+    snapshot_layouts();
 }
 
 namespace {
@@ -405,7 +417,7 @@ void make_kernel_edges_programmatic(cudaGraph_t g) {
 
 }  // namespace
 
-void GraphProcess::capture() {
+void GraphProcess::capture(bool update) {
     CudaBackend& cb = session().cuda();
     cb.make_current();
     cudaStream_t cs = nullptr;
@@ -429,6 +441,16 @@ void GraphProcess::capture() {
     } catch (...) {
         cudaGraphDestroy(g);
         throw;
+    }
+    if (update && exec_) {
+        // same topology, new pointers: patch the kernel node params in place
+        cudaGraphExecUpdateResultInfo info{};
+        if (cudaGraphExecUpdate(exec_, g, &info) == cudaSuccess) {
+            if (graph_) cudaGraphDestroy(graph_);
+            graph_ = g;
+            return;
+        }
+        cudaGetLastError();  // topology changed: instantiate afresh below
     }
     cudaGraphExec_t x = nullptr;
     const cudaError_t ei = cudaGraphInstantiate(&x, g, 0);
@@ -586,6 +608,10 @@ public:
         in_ = session().device_array(require_input(), 0);
         out_ = session().device_array(require_output(), 0);
     }
+    void repoint() override {
+        in_ = session().device_array(require_input(), 0);
+        out_ = session().device_array(require_output(), 0);
+    }
     void record(cudaStream_t s) override {
         ck(dev::launch_negate(type_, in_, out_, n_, mv_, s), name());
         mark(s);
@@ -658,6 +684,10 @@ public:
         else
             plan_.make(nx_, ny_, inverse_ ? 1 : -1, batch_, dev::Combine::None, ny_ * batch_,
                        session().cuda().ordinal());
+    }
+    void repoint() override {
+        in_ = static_cast<const float2*>(session().device_array(require_input(), 0));
+        out_ = static_cast<float2*>(session().device_array(require_output(), 0));
     }
     void record(cudaStream_t s) override {
         if (radix2_) {
@@ -813,6 +843,7 @@ public:
         }
         params_ = upload_bytes(&param_word, sizeof param_word);
     }
+    void repoint() override {}  // record() reads the pointers and headers itself
     void record(cudaStream_t s) override {
         hetreco_kernel_args a{};
         a.in = session().device_array(require_input(), 0);
@@ -979,6 +1010,13 @@ public:
             }
         }
     }
+    void repoint() override {
+        y_ = static_cast<const float2*>(session().device_array(require_input(), 0));
+        if (mode_ == dev::Combine::Sense) smap_ = static_cast<const float2*>(session().device_array(require_input(), 1));
+        out_ = session().device_array(require_output(), 0);
+        if (cluster_)
+            ck(dev::make_cluster_map(cmap_, y_, ny_ * nc_ * nf_, cplan_.cl), name() + ": TMA descriptor");
+    }
     void record(cudaStream_t s) override {
         const float scale = float(1.0 / (double(nx_) * double(ny_)));
         if (cluster_) {
@@ -1133,6 +1171,12 @@ public:
                           : combine_ss_enabled(nx_) ? dev::plan_combine_ss(nx_, ny_, nf_, sms)
                                                     : dev::plan_contig(nx_, dev::Combine::Sense, ny_ * nf_, sms);
         }
+    }
+    void repoint() override {
+        m_ = static_cast<const float2*>(session().device_array(require_input(), 0));
+        s_ = static_cast<const float2*>(session().device_array(require_input(), 1));
+        if (mask_) mask_ = static_cast<const float*>(session().device_array(require_input(), 2));
+        out_ = static_cast<float2*>(session().device_array(require_output(), 0));
     }
     void record(cudaStream_t s) override {
         float2* z = normal_ ? scratch_.as<float2>() : out_;

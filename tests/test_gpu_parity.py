@@ -812,3 +812,40 @@ def test_chain_failure_leaves_stages_usable(s):
     c = h.chain(s, "ok", [p1, p2])  # still chainable after the failures
     c.init().launch()
     assert beq(s.fetch_data(hb).arrays[0], o.negate(o.negate(x, 1.0), 1.0))
+
+
+def test_repoint_same_shapes_patches_graph(s):
+    """set_input/set_output after init with the same shapes re-points the
+    baked plan (cudaGraphExecUpdate, no rebake) -- results follow the new
+    handles; a shape change still re-validates and re-plans."""
+    rng = np.random.default_rng(17)
+    nx, nc, nf = 128, 4, 3
+    Ys = [cplx(rng, nx, nx, nc, nf) for _ in range(2)]
+    S = cplx(rng, nx, nx, nc)
+    hins = [s.register_data(h.Data([Y, S], h.DataKind.KData)) for Y in Ys]
+    houts = [s.allocate_data([((nx, nx, nf), np.complex64)], h.DataKind.XData) for _ in range(2)]
+    refs = [o.sens_recon(Y, S) for Y in Ys]
+    p = h.Process(s, "sens_recon").set_input(hins[0]).set_output(houts[0]).init()
+    for it in range(6):
+        i, k = it % 2, (it // 2) % 2
+        p.set_input(hins[i]).set_output(houts[k])
+        p.launch()
+        assert relmax(s.fetch_data(houts[k]).arrays[0], refs[i]) <= TOL
+    # negate re-pointed between two images, and fft2d
+    xs = [np.asfortranarray(rng.random((64, 64), dtype=np.float32)) for _ in range(2)]
+    hx = [s.register_data([x]) for x in xs]
+    hy = s.allocate_data([((64, 64), np.float32)])
+    q = h.Process(s, "negate").set_input(hx[0]).set_output(hy).init({"max_value": 1.0})
+    for i in (1, 0, 1):
+        q.set_input(hx[i])
+        q.launch()
+        assert beq(s.fetch_data(hy).arrays[0], o.negate(xs[i], 1.0))
+    # shape change: 5 frames instead of 3 -> full re-plan, still correct
+    Y5 = cplx(rng, nx, nx, nc, 5)
+    h5 = s.register_data(h.Data([Y5, S], h.DataKind.KData))
+    o5 = s.allocate_data([((nx, nx, 5), np.complex64)], h.DataKind.XData)
+    p.set_input(h5).set_output(o5)
+    p.launch()
+    assert relmax(s.fetch_data(o5).arrays[0], o.sens_recon(Y5, S)) <= TOL
+    for hd in hins + houts + hx + [hy, h5, o5]:
+        s.release_data(hd)
