@@ -35,7 +35,8 @@ typedef struct CUlib_st* cudaLibrary_t;
 namespace hetreco {
 
 namespace detail {
-class HostStager;  // pinned-ring staging of pageable transfers (csrc/host/host_stager.hpp)
+class HostStager;         // pinned-ring staging of pageable transfers (csrc/host/host_stager.hpp)
+class FusedReconKernels;  // sens_recon / rss_recon as layer-1 kernels (csrc/host/fused_recon.hpp)
 }
 
 // ---- devices (device.hpp:15-114) ---------------------------------------------------
@@ -242,6 +243,11 @@ private:
     // pageable host <-> device transfers through a pinned ring (lazily built)
     mutable std::unique_ptr<detail::HostStager> stager_;
     detail::HostStager& stager() const;
+    // host copies of small buffers uploaded whole (layout headers): execute()
+    // of the fused kernels reads the shapes without a device round trip
+    std::unordered_map<BufferId, std::vector<std::byte>> shadow_;
+    LayoutDescriptor header_layout(BufferId header) const;
+    std::unique_ptr<detail::FusedReconKernels> fused_;
     // run-time compiled (NVRTC) kernels: "<unit tag>/<name>" -> entry point
     std::unordered_map<std::string, cudaKernel_t> jit_;
     std::vector<cudaLibrary_t> jit_libs_;
@@ -250,5 +256,11 @@ private:
 
 // Number of CUDA devices visible to this process (0 when no driver/GPU).
 int cuda_device_count();
+
+// The intrinsic kernel bundle of CudaBackend: the six reference-ABI builtins
+// (kernels/*.cl.src semantics) then the fused "sens_recon" / "rss_recon"
+// chains (csrc/host/fused_recon.hpp).  nullptr past the end.
+int intrinsic_kernel_count();
+const char* intrinsic_kernel_name(int index);
 
 }  // namespace hetreco

@@ -19,6 +19,7 @@
 
 #include "hetreco/backend.hpp"
 #include "hetreco/errors.hpp"
+#include "hetreco/kernels.hpp"
 #include "hetreco_b200.h"
 
 namespace hetreco_b200_integration {
@@ -133,7 +134,28 @@ public:
             }
         }
         if (!failures.empty()) throw CompileError(std::move(failures));
+        // The reference's builtin bundle (kernels.hpp:52-57) compiled from
+        // source: append the precompiled fused chains (sens_recon, rss_recon;
+        // csrc/host/fused_recon.hpp), which have no kernel-source form, so
+        // load_builtin_kernels (session.cpp:139-148) registers them in both modes.
+        if (is_builtin_bundle(units)) {
+            int n = 0;
+            ck(hetreco_cuda_kernel_count(&n));
+            for (int i = 0; i < n; ++i) {
+                const std::string name = hetreco_cuda_kernel_name(i);
+                bool have = false;
+                for (const CompiledKernel& k : out) have = have || k.name == name;
+                if (!have) out.push_back({name, "sm_100a:" + name, &device_only});
+            }
+        }
         return out;
+    }
+    static bool is_builtin_bundle(std::span<const ProgramSource> units) {
+        const auto builtins = builtin_kernel_sources();
+        if (units.size() != builtins.size()) return false;
+        for (std::size_t i = 0; i < units.size(); ++i)
+            if (units[i].unit_name != builtins[i].unit_name) return false;
+        return true;
     }
     void execute(const CompiledKernel& k, const KernelBinding& b, std::uint64_t gsize) override {
         if (k.unit_name.rfind("nvrtc#", 0) == 0) {

@@ -240,12 +240,12 @@ int hetreco_cuda_copy(hetreco_cuda_backend b, uint64_t src, uint64_t so, uint64_
 int hetreco_cuda_kernel_count(int* count) {
     return guard([&] {
         need(count, "count");
-        *count = int(dev::Builtin::Count);
+        *count = intrinsic_kernel_count();
     });
 }
 
 const char* hetreco_cuda_kernel_name(int i) {
-    return (i >= 0 && i < int(dev::Builtin::Count)) ? dev::builtin_name(dev::Builtin(i)) : nullptr;
+    return intrinsic_kernel_name(i);
 }
 
 int hetreco_cuda_execute(hetreco_cuda_backend b, const char* name, uint64_t in, uint64_t inh, uint64_t out,

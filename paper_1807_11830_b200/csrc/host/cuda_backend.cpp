@@ -4,12 +4,14 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <set>
 
 #include "../kernels/launch.hpp"
 #include "hetreco_b200/runtime.hpp"
 
+#include "fused_recon.hpp"
 #include "host_stager.hpp"
 #include "nvrtc_compiler.hpp"
 
@@ -109,6 +111,7 @@ CudaBackend::~CudaBackend() {
     cudaStreamDestroy(h2d_);
     cudaStreamDestroy(d2h_);
     for (cudaLibrary_t l : jit_libs_) cudaLibraryUnload(l);
+    fused_.reset();
     stager_.reset();
 }
 
@@ -157,6 +160,7 @@ void CudaBackend::release(BufferId id) {
     // stream-ordered: in-flight work on the compute stream finishes first
     cudaFreeAsync(it->second.ptr, compute_);
     note_work();
+    shadow_.erase(id);
     used_ -= it->second.size;
     bufs_.erase(it);
 }
@@ -167,7 +171,13 @@ void CudaBackend::release(BufferId id) {
 constexpr std::size_t kStageMin = std::size_t(4) << 20;
 
 detail::HostStager& CudaBackend::stager() const {
-    if (!stager_) stager_ = std::make_unique<detail::HostStager>(ordinal_);
+    if (!stager_) {
+        // experiment knobs: HETRECO_STAGER_SLOT_MB (16), HETRECO_STAGER_SLOTS (3)
+        const char* mb = std::getenv("HETRECO_STAGER_SLOT_MB");
+        const char* k = std::getenv("HETRECO_STAGER_SLOTS");
+        const std::size_t slot = std::size_t(mb && *mb ? std::max(1, std::atoi(mb)) : 16) << 20;
+        stager_ = std::make_unique<detail::HostStager>(ordinal_, slot, k && *k ? std::max(2, std::atoi(k)) : 3);
+    }
     return *stager_;
 }
 
@@ -176,6 +186,12 @@ void CudaBackend::upload(BufferId id, std::uint64_t off, std::span<const std::by
     const Buf& b = lookup(id);
     check_window("upload", off, bytes.size(), b.size);
     if (bytes.empty()) return;
+    constexpr std::uint64_t kShadowMax = 4096;  // layout headers are (1 + 11 A) * 8 bytes
+    if (b.size <= kShadowMax) {
+        auto& sh = shadow_[id];
+        sh.resize(b.size);  // a fresh buffer is zero-filled, like the device copy
+        std::memcpy(sh.data() + off, bytes.data(), bytes.size());
+    }
     make_current();
     note_work();
     if (bytes.size() >= kStageMin && !detail::HostStager::is_pinned(bytes.data())) {
@@ -226,6 +242,7 @@ void CudaBackend::copy(BufferId src, std::uint64_t so, BufferId dst, std::uint64
     if (n == 0) return;
     make_current();
     note_work();
+    shadow_.erase(dst);
     ck(cudaMemcpyAsync(static_cast<char*>(d.ptr) + doff, static_cast<const char*>(s.ptr) + so, n,
                        cudaMemcpyDeviceToDevice, compute_),
        "cudaMemcpyAsync(D2D)");
@@ -233,11 +250,30 @@ void CudaBackend::copy(BufferId src, std::uint64_t so, BufferId dst, std::uint64
 
 std::vector<CompiledKernel> CudaBackend::intrinsic_kernels() {
     std::vector<CompiledKernel> ks;
-    for (int i = 0; i < int(dev::Builtin::Count); ++i) {
-        const char* n = dev::builtin_name(dev::Builtin(i));
+    for (int i = 0; i < intrinsic_kernel_count(); ++i) {
+        const char* n = intrinsic_kernel_name(i);
         ks.push_back({n, std::string("sm_100a:") + n, &device_only_entry});
     }
     return ks;
+}
+
+int intrinsic_kernel_count() { return int(dev::Builtin::Count) + 2; }
+
+const char* intrinsic_kernel_name(int i) {
+    if (i >= 0 && i < int(dev::Builtin::Count)) return dev::builtin_name(dev::Builtin(i));
+    if (i == int(dev::Builtin::Count)) return detail::FusedReconKernels::kSense;
+    if (i == int(dev::Builtin::Count) + 1) return detail::FusedReconKernels::kRss;
+    return nullptr;
+}
+
+LayoutDescriptor CudaBackend::header_layout(BufferId header) const {
+    auto it = shadow_.find(header);
+    if (it != shadow_.end()) return parse_layout_header(it->second);
+    const Buf& b = lookup(header);  // not uploaded whole from the host: read it back
+    std::vector<std::byte> bytes(b.size);
+    ck(cudaMemcpyAsync(bytes.data(), b.ptr, b.size, cudaMemcpyDeviceToHost, compute_), "cudaMemcpyAsync(header)");
+    ck(cudaStreamSynchronize(compute_), "cudaStreamSynchronize(header)");
+    return parse_layout_header(bytes);
 }
 
 bool CudaBackend::supports_source_kernels() const { return nvrtc::available(); }
@@ -316,6 +352,21 @@ void CudaBackend::execute(const CompiledKernel& kernel, const KernelBinding& bin
         auto it = jit_.find(kernel.unit_name + "/" + kernel.name);
         if (it == jit_.end()) throw DeviceError(kernel.name, "kernel was compiled by another backend");
         jit = it->second;
+    }
+    if (!jit && detail::FusedReconKernels::is_fused(kernel.name)) {
+        // fused IFFT2 + coil combine (fused_recon.hpp): shapes from the headers
+        const Buf& in = lookup(bind.input);
+        const Buf& out = lookup(bind.output);
+        const LayoutDescriptor li = header_layout(bind.input_header);
+        const LayoutDescriptor lo = header_layout(bind.output_header);
+        for (const LayoutRecord& r : li.records) check_window("sens/rss_recon input array", r.offset_bytes, r.byte_size(), in.size);
+        for (const LayoutRecord& r : lo.records) check_window("sens/rss_recon output array", r.offset_bytes, r.byte_size(), out.size);
+        make_current();
+        if (!fused_) fused_ = std::make_unique<detail::FusedReconKernels>(ordinal_);
+        last_kernel_ = kernel.name;
+        note_work();
+        fused_->launch(kernel.name, li, lo, in.ptr, out.ptr, bind.params, gsize, compute_);
+        return;
     }
     const int which = jit ? -1 : dev::builtin_from_name(kernel.name.c_str());
     if (!jit && which < 0) throw DeviceError(kernel.name, "no sm_100a implementation registered under this name");

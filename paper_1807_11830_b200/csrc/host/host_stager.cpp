@@ -1,7 +1,11 @@
 // host_stager.cpp -- see host_stager.hpp.
 #include "host_stager.hpp"
 
+#include <emmintrin.h>
+
 #include <algorithm>
+#include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -24,6 +28,39 @@ namespace {
 // Bytes per part, rounded up to a cache line; parts * result >= n for every n.
 std::size_t part_bytes(std::size_t n, unsigned parts) {
     return ((n + parts - 1) / parts + 63) & ~std::size_t(63);
+}
+
+// Streaming (non-temporal) stores for the staging copies: the destination is
+// consumed by the copy engine or by the caller much later, so write-allocating
+// it in the cache only adds a read-for-ownership per line to a copy that is
+// host-memory-bandwidth bound next to the concurrent DMA.  HETRECO_STAGER_NT=0
+// falls back to memcpy (A/B runs).
+bool nt_enabled() {
+    static const bool on = [] {
+        const char* v = std::getenv("HETRECO_STAGER_NT");
+        return !(v && *v == '0');
+    }();
+    return on;
+}
+
+void copy_part(char* d, const char* s, std::size_t n) {
+    if (!nt_enabled() || n < 4096 || (reinterpret_cast<std::uintptr_t>(d) & 15)) {
+        std::memcpy(d, s, n);
+        return;
+    }
+    std::size_t i = 0;
+    for (; i + 64 <= n; i += 64) {
+        const __m128i a = _mm_loadu_si128(reinterpret_cast<const __m128i*>(s + i));
+        const __m128i b = _mm_loadu_si128(reinterpret_cast<const __m128i*>(s + i + 16));
+        const __m128i c = _mm_loadu_si128(reinterpret_cast<const __m128i*>(s + i + 32));
+        const __m128i e = _mm_loadu_si128(reinterpret_cast<const __m128i*>(s + i + 48));
+        _mm_stream_si128(reinterpret_cast<__m128i*>(d + i), a);
+        _mm_stream_si128(reinterpret_cast<__m128i*>(d + i + 16), b);
+        _mm_stream_si128(reinterpret_cast<__m128i*>(d + i + 32), c);
+        _mm_stream_si128(reinterpret_cast<__m128i*>(d + i + 48), e);
+    }
+    if (i < n) std::memcpy(d + i, s + i, n - i);
+    _mm_sfence();  // the stores are globally visible before the DMA is enqueued
 }
 }  // namespace
 
@@ -59,7 +96,7 @@ void CopyPool::run(unsigned index) {
         const unsigned parts = size();
         const std::size_t per = part_bytes(n, parts);
         const std::size_t b = std::min(n, per * index), e = std::min(n, b + per);
-        if (e > b) std::memcpy(d + b, s + b, e - b);
+        if (e > b) copy_part(d + b, s + b, e - b);
         {
             std::lock_guard lk(mu_);
             if (--pending_ == 0) done_.notify_one();
@@ -69,7 +106,7 @@ void CopyPool::run(unsigned index) {
 
 void CopyPool::copy(void* dst, const void* src, std::size_t n) {
     if (workers_.empty() || n < (std::size_t(1) << 20)) {
-        std::memcpy(dst, src, n);
+        copy_part(static_cast<char*>(dst), static_cast<const char*>(src), n);
         return;
     }
     {
@@ -83,16 +120,23 @@ void CopyPool::copy(void* dst, const void* src, std::size_t n) {
     go_.notify_all();
     const unsigned parts = size();
     const std::size_t per = part_bytes(n, parts);
-    std::memcpy(dst, src, std::min(n, per));  // the caller's share (part 0)
+    copy_part(static_cast<char*>(dst), static_cast<const char*>(src), std::min(n, per));  // the caller's share (part 0)
     std::unique_lock lk(mu_);
     done_.wait(lk, [&] { return pending_ == 0; });
 }
 
 // ---- HostStager ---------------------------------------------------------------------------
 
+// memcpy threads of the staging pool: half the host's hardware threads, at
+// most 8 (HETRECO_STAGER_THREADS overrides, for A/B runs).
+unsigned copy_threads() {
+    if (const char* v = std::getenv("HETRECO_STAGER_THREADS"); v && *v) return unsigned(std::max(1, std::atoi(v)));
+    return std::max(1u, std::min(8u, std::thread::hardware_concurrency() / 2));
+}
+
 HostStager::HostStager(int device, std::size_t slot_bytes, int slots)
     : device_(device), slot_(slot_bytes),
-      pool_(std::max(1u, std::min(8u, std::thread::hardware_concurrency() / 2))) {
+      pool_(copy_threads()) {
     cudaSetDevice(device_);
     for (int i = 0; i < slots; ++i) {
         std::byte* p = nullptr;

@@ -11,6 +11,7 @@
 #include <cstring>
 
 #include "../kernels/launch.hpp"
+#include "fused_recon.hpp"
 
 namespace hetreco {
 
@@ -38,6 +39,18 @@ bool combine_ss_enabled(std::uint64_t nx) {
     if (e && *e == '0') return false;
     if (!dev::combine_ss_supported(nx)) return false;
     return (e && *e == '1') || (nx >= 64 && nx <= 512 && is_pow2(nx));
+}
+
+// The measured default axis-0 + combine kernel for a fp32 SENSE/RSS chunk of
+// `frames` frames: coil-parallel when the coil-serial kernel would leave the
+// SMs short of lines (few frames), the staged-map SENSE kernel where it
+// measured faster, else the register-prefetch kernel (variant 11: fp32,
+// prefetch, register copy; ping-pong at 512).
+dev::LaunchShape plan_combine_fp32(std::uint64_t nx, std::uint64_t ny, std::uint64_t nc, std::uint64_t frames,
+                                   dev::Combine mode, int sms) {
+    if (dev::combine_cp_preferred(nx, ny * frames, nc, sms)) return dev::plan_combine_cp(nx, mode, ny * frames, sms);
+    if (mode == dev::Combine::Sense && combine_ss_enabled(nx)) return dev::plan_combine_ss(nx, ny, frames, sms);
+    return dev::plan_contig(nx, mode, ny * frames, sms);
 }
 
 // Owning device allocation on the session's GPU.
@@ -1364,6 +1377,89 @@ void StreamingRecon::run(const void* host_in, std::uint64_t frames, void* host_o
     const cudaError_t e = cudaStreamSynchronize(ds);
     if (e != cudaSuccess) throw DeviceError("streaming_recon", cudaGetErrorString(e));
     ck(cudaStreamSynchronize(cs), "streaming recon (compute)");
+}
+
+// ---- fused recon as layer-1 kernels (detail::FusedReconKernels) -----------------------------
+
+struct detail::FusedReconKernels::Plan {
+    DevMem tw_x, tw_y;
+    dev::LaunchShape s1, s2;
+};
+
+detail::FusedReconKernels::FusedReconKernels(int ordinal) : ordinal_(ordinal) {}
+
+detail::FusedReconKernels::~FusedReconKernels() {
+    if (scratch_) cudaFree(scratch_);
+}
+
+bool detail::FusedReconKernels::is_fused(std::string_view name) { return name == kSense || name == kRss; }
+
+void detail::FusedReconKernels::launch(std::string_view name, const LayoutDescriptor& li, const LayoutDescriptor& lo,
+                                       const void* in_base, void* out_base, std::span<const std::byte> params,
+                                       std::uint64_t gsize, cudaStream_t stream) {
+    const bool sense = name == kSense;
+    const std::string who(name);
+    const dev::Combine mode = sense ? dev::Combine::Sense : dev::Combine::Rss;
+    std::uint32_t flags = 0;
+    if (!params.empty()) {
+        if (params.size() != 4) throw InvalidArgument(who + ": params are empty or one u32 flag word (bit 0 = shift)");
+        std::memcpy(&flags, params.data(), 4);
+        if (flags & ~1u) throw InvalidArgument(who + ": unknown flag bits in params");
+    }
+    const LayoutRecord& y = array_of(li, 0, who);
+    require_type(y, ElementType::Complex64, who);
+    if (y.rank < 3) throw ShapeMismatch(who + ": k-space must be [nx, ny, coils(, frames)], got " + dims_str(y));
+    const std::uint64_t nx = y.dims[0], ny = y.dims[1], nc = y.dims[2], nf = prod(y, 3, y.rank);
+    if (!dev::fft_size_supported(nx) || !dev::fft_size_supported(ny))
+        throw ShapeMismatch(who + ": spatial dims must be powers of two <= 4096 or mixed-radix sides, got " + dims_str(y));
+    const LayoutRecord& o = array_of(lo, 0, who);
+    require_type(o, sense ? ElementType::Complex64 : ElementType::Float32, who);
+    if (o.dims[0] != nx || (o.rank > 1 ? o.dims[1] : 1) != ny || o.element_count() != nx * ny * nf)
+        throw ShapeMismatch(who + ": output " + dims_str(o) + " must be [nx, ny, frames] for k-space " + dims_str(y));
+    // one work item per output pixel, as the reference's combine kernels
+    if (gsize != nx * ny * nf)
+        throw InvalidArgument(who + ": global size must be nx*ny*frames = " + std::to_string(nx * ny * nf) + ", got " +
+                              std::to_string(gsize));
+    const float2* smap = nullptr;
+    if (sense) {
+        const LayoutRecord& sm = array_of(li, 1, who);
+        require_type(sm, ElementType::Complex64, who);
+        if (sm.dims[0] != nx || sm.dims[1] != ny || sm.element_count() != nx * ny * nc)
+            throw ShapeMismatch(who + ": sensitivity maps " + dims_str(sm) + " must be [nx, ny, coils]");
+        smap = reinterpret_cast<const float2*>(static_cast<const char*>(in_base) + sm.offset_bytes);
+    }
+    const auto* ydev = reinterpret_cast<const float2*>(static_cast<const char*>(in_base) + y.offset_bytes);
+    void* out = static_cast<char*>(out_base) + o.offset_bytes;
+    const std::string key = who + ":" + std::to_string(nx) + "x" + std::to_string(ny) + "x" + std::to_string(nc) + "x" +
+                            std::to_string(nf);
+    auto it = plans_.find(key);
+    if (it == plans_.end()) {
+        auto pl = std::make_unique<Plan>();
+        const int sms = sm_count(ordinal_);
+        pl->tw_y = twiddle_table(ny, +1);
+        pl->tw_x = twiddle_table(nx, +1);
+        pl->s1 = dev::plan_strided(ny, nx, nc * nf, sms);
+        pl->s2 = plan_combine_fp32(nx, ny, nc, nf, mode, sms);
+        it = plans_.emplace(key, std::move(pl)).first;
+    }
+    const Plan& pl = *it->second;
+    const std::uint64_t need = nx * ny * nc * nf * 8;
+    if (need > scratch_bytes_) {
+        // earlier launches on this stream may still read the old scratch
+        ck(cudaStreamSynchronize(stream), who + ": scratch resize");
+        if (scratch_) cudaFree(scratch_);
+        scratch_ = nullptr;
+        scratch_bytes_ = 0;
+        ck(cudaMalloc(&scratch_, need), who + ": scratch");
+        scratch_bytes_ = need;
+    }
+    const bool shift = flags & 1u;
+    auto* x = static_cast<float2*>(scratch_);
+    dev::StridedArgs a1{ydev, x, nx, nc * nf, shift, shift, 1.0f, pl.tw_y.as<float2>()};
+    ck(dev::launch_strided(ny, +1, a1, pl.s1, stream), who + "/axis1");
+    dev::ContigArgs a2{x, out, smap, ny, nc, nf, shift, shift, float(1.0 / (double(nx) * double(ny))),
+                       pl.tw_x.as<float2>()};
+    ck(dev::launch_contig(nx, +1, mode, a2, pl.s2, stream), who + "/axis0+combine");
 }
 
 }  // namespace hetreco

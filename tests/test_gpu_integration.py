@@ -67,3 +67,29 @@ def test_reference_recon_chain_on_b200_bitexact(method, source_mode):
     S = cplx(rng, 128, 64, 8) if method == "sens" else None
     cpu, gpu = both(lambda: o.ref_recon(method, Y, S)[0], source_mode)
     assert beq(cpu, gpu)
+
+
+def relmax(a, ref):
+    return float(np.abs(np.asarray(a) - ref).max() / max(float(np.abs(ref).max()), 1e-30))
+
+
+@pytest.mark.parametrize("method", ["sens", "rss"])
+def test_reference_session_launches_fused_recon_on_b200(method, source_mode):
+    """The unmodified reference ComputeSession reaches the fused B200 chain:
+    load_builtin_kernels registers "sens_recon" / "rss_recon" from the
+    adapter's intrinsic bundle (precompiled mode) or next to the NVRTC-built
+    builtins (source mode), and launch_kernel([Y, S] -> [M]) runs the two
+    fused kernels instead of the 20-launch radix-2 chain.  Within the
+    north_star 1e-5 of the reference CPU chain (fp32 coil accumulation)."""
+    rng = np.random.default_rng(8)
+    nx, ny, nc, nf = 256, 128, 8, 3
+    Y = cplx(rng, nx, ny, nc, nf)
+    S = cplx(rng, nx, ny, nc) if method == "sens" else None
+    ref = o.ref_recon(method, Y, S)[0]  # reference chain on its CPU backend
+    kernel = "sens_recon" if method == "sens" else "rss_recon"
+    out = np.zeros((nx, ny, nf), np.complex64 if method == "sens" else np.float32, order="F")
+    with o.use_reference_on_b200(source_mode):
+        got = o.ref_run_kernel(kernel, Y, b"", nx * ny * nf, out_like=out, extra=S)
+    assert relmax(got, ref) <= 1e-5
+    with pytest.raises(Exception):  # the CPU reference backend has no such kernel
+        o.ref_run_kernel(kernel, Y, b"", nx * ny * nf, out_like=out, extra=S)

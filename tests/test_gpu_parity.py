@@ -115,10 +115,10 @@ def test_backend_capacity_and_ranges():
 
 def test_builtin_registry(s):
     assert set(s.kernel_names()) == {"negate", "fft_radix2_pass", "complex_element_prod", "ximage_sum",
-                                     "rss_combine", "matrix_add"}
+                                     "rss_combine", "matrix_add", "sens_recon", "rss_recon"}
     with pytest.raises(h.CompileError):  # source units go to NVRTC (tests/test_source_kernels.py)
         s.load_kernels([("broken.cl.src", "this is not a kernel")])
-    assert len(s.kernel_names()) == 6
+    assert len(s.kernel_names()) == 8
     hd = s.register_data([np.zeros(4, np.float32)])
     with pytest.raises(h.UnknownKernel):
         s.launch_kernel("nonexistent", hd, hd, b"", 4)
@@ -849,3 +849,32 @@ def test_repoint_same_shapes_patches_graph(s):
     assert relmax(s.fetch_data(o5).arrays[0], o.sens_recon(Y5, S)) <= TOL
     for hd in hins + houts + hx + [hy, h5, o5]:
         s.release_data(hd)
+
+
+@pytest.mark.parametrize("shift", [False, True])
+def test_fused_recon_as_abi_kernels(s, shift):
+    """"sens_recon" / "rss_recon" in the layer-1 kernel table (fused_recon.hpp):
+    launch_kernel over [Y, S] -> [M] equals the layer-2 process; shape,
+    global-size and params errors are reported."""
+    rng = np.random.default_rng(23)
+    nx, ny, nc, nf = 128, 64, 5, 3
+    Y = cplx(rng, nx, ny, nc, nf)
+    S = cplx(rng, nx, ny, nc)
+    flags = struct.pack("<I", int(shift))
+    M = launch_one(s, "sens_recon", [Y, S], np.zeros((nx, ny, nf), np.complex64, order="F"), flags, nx * ny * nf)
+    R = launch_one(s, "rss_recon", [Y], np.zeros((nx, ny, nf), np.float32, order="F"), flags, nx * ny * nf)
+    (Mp,), _ = run_process(s, "sens_recon", [Y, S], [((nx, ny, nf), np.complex64)], {"shift": shift})
+    (Rp,), _ = run_process(s, "rss_recon", [Y], [((nx, ny, nf), np.float32)], {"shift": shift})
+    assert beq(M, Mp) and beq(R, Rp)
+    if not shift:
+        assert relmax(M, o.sens_recon(Y, S)) <= TOL
+        assert relmax(R, o.rss_recon(Y)) <= TOL
+    out = np.zeros((nx, ny, nf), np.complex64, order="F")
+    with pytest.raises(h.InvalidArgument):  # global size is one item per output pixel
+        launch_one(s, "sens_recon", [Y, S], out, b"", 7)
+    with pytest.raises(h.InvalidArgument):
+        launch_one(s, "sens_recon", [Y, S], out, b"\x01\x00", nx * ny * nf)
+    with pytest.raises(h.ShapeMismatch):
+        launch_one(s, "sens_recon", [Y, S], np.zeros((nx, ny, nf + 1), np.complex64, order="F"), b"", nx * ny * (nf + 1))
+    with pytest.raises(h.HetrecoError):  # SENSE needs the maps array
+        launch_one(s, "sens_recon", [Y], out, b"", nx * ny * nf)

@@ -124,4 +124,5 @@ def test_no_gpu_means_no_device_and_no_fallback():
 
 def test_intrinsic_kernel_names():
     assert h.CudaBackend.intrinsic_kernel_names() == [
-        "negate", "fft_radix2_pass", "complex_element_prod", "ximage_sum", "rss_combine", "matrix_add"]
+        "negate", "fft_radix2_pass", "complex_element_prod", "ximage_sum", "rss_combine", "matrix_add",
+        "sens_recon", "rss_recon"]
