@@ -174,6 +174,7 @@ bool combine_ss_supported(std::uint64_t N) {
 
 LaunchShape plan_combine_ss(std::uint64_t N, std::uint64_t ny, std::uint64_t frames, int sms) {
     LaunchShape s;
+    if (combine_tc_enabled(N)) return plan_combine_tc(N, ny, frames, sms);  // experiment (profiles/round2_dft_gemm.md)
     switch (N) {
 #define X(n) \
     case n: s = plan_ss_n<n>(ny, frames, sms); break;

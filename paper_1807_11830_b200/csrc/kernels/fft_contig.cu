@@ -74,6 +74,7 @@ cudaError_t launch_contig(std::uint64_t N, int dir, Combine mode, const ContigAr
     if (mode != Combine::None) {
         if (dir < 0) return cudaErrorInvalidValue;
         if (s.variant & 128) return launch_combine_cp(N, mode, a, s, st);
+        if (s.variant & 512) return mode == Combine::Sense ? launch_combine_tc(N, a, s, st) : cudaErrorInvalidValue;
         if (s.variant & 256) return mode == Combine::Sense ? launch_combine_ss(N, a, s, st) : cudaErrorInvalidValue;
         return combine_launch(mode, N, s.variant, a, s, lpb, items, st);
     }

@@ -113,6 +113,13 @@ bool combine_ss_supported(std::uint64_t N);
 LaunchShape plan_combine_ss(std::uint64_t N, std::uint64_t ny, std::uint64_t frames, int device_sms);
 cudaError_t launch_combine_ss(std::uint64_t N, const ContigArgs& a, const LaunchShape& s, cudaStream_t stream);
 
+// ---- SENSE combine with the 16 x 16 DFT stages on tcgen05 (fft_combine_tc.cu) ------
+// 256-point lines only; HETRECO_COMBINE_TC=1 selects it in place of the
+// staged-map kernel (plan_combine_ss returns its shape, variant bit 512).
+bool combine_tc_enabled(std::uint64_t N);
+LaunchShape plan_combine_tc(std::uint64_t N, std::uint64_t ny, std::uint64_t frames, int device_sms);
+cudaError_t launch_combine_tc(std::uint64_t N, const ContigArgs& a, const LaunchShape& s, cudaStream_t stream);
+
 // ---- axis-0 + combine fed by a TMA bulk-copy ring (fft_combine_tma.cu) -----------
 // Same contract as launch_contig with mode Sense/Rss and fp32 accumulation;
 // a.in = X [N, ny, C, F].  HETRECO_TMA_STAGES (2|3|4|6, default 4) = tiles in
