@@ -1176,8 +1176,10 @@ public:
         } else {
             s_col_ = dev::plan_strided_masked(ny_, normal_, nc_ * nf_, sms);
         }
+        fused_ = dev::LaunchShape{};
         if (normal_) {
             tw_inv_ = twiddle_table(nx_, +1);
+            fused_ = dev::plan_sense_normal_fused(nx_, nc_ * nf_, sms);
             if (scratch_.size() != nx_ * ny_ * nc_ * nf_ * 8) scratch_ = DevMem(nx_ * ny_ * nc_ * nf_ * 8);
             s_comb_ = dev::combine_cp_preferred(nx_, ny_ * nf_, nc_, sms)
                           ? dev::plan_combine_cp(nx_, dev::Combine::Sense, ny_ * nf_, sms)
@@ -1193,6 +1195,15 @@ public:
     }
     void record(cudaStream_t s) override {
         float2* z = normal_ ? scratch_.as<float2>() : out_;
+        if (normal_ && fused_.block) {  // one cooperative kernel, three grid-barrier phases
+            dev::SenseNormalArgs an{m_, s_, mask_, z, out_, tw_fwd_.as<float2>(), tw_inv_.as<float2>(),
+                                    std::uint32_t(nc_), std::uint32_t(nf_), shift_,
+                                    float(1.0 / (double(nx_) * double(ny_)))};
+            an.phases = int(env_or("HETRECO_NORMAL_PHASES", 7));
+            ck(dev::launch_sense_normal_fused(nx_, an, fused_, s), name() + "/normal-fused");
+            mark(s);
+            return;
+        }
         dev::ContigArgs ae{m_, z, s_, ny_, nc_, nf_, shift_, shift_, 1.0f, tw_fwd_.as<float2>()};
         ck(dev::launch_expand(nx_, ae, s_exp_, s), name() + "/expand+x-fft");
         mark(s);
@@ -1222,7 +1233,7 @@ private:
     const float* mask_ = nullptr;
     float2* out_ = nullptr;
     DevMem tw_fwd_, tw_fwd_y_, tw_inv_, scratch_;
-    dev::LaunchShape s_exp_, s_col_, s_comb_;
+    dev::LaunchShape s_exp_, s_col_, s_comb_, fused_;
     bool generic_cols_ = false;
 };
 

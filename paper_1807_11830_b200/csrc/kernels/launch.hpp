@@ -120,6 +120,28 @@ bool combine_tc_enabled(std::uint64_t N);
 LaunchShape plan_combine_tc(std::uint64_t N, std::uint64_t ny, std::uint64_t frames, int device_sms);
 cudaError_t launch_combine_tc(std::uint64_t N, const ContigArgs& a, const LaunchShape& s, cudaStream_t stream);
 
+// ---- SENSE normal operator E^H E in one cooperative kernel (fft_sense_normal.cu) --
+// Square power-of-two sides 64..256; three phases separated by grid barriers.
+// Opt-in (HETRECO_NORMAL_FUSED=1; measured slower than the three-kernel graph);
+// plan returns block == 0 otherwise.
+struct SenseNormalArgs {
+    const float2* m;     // image [N, N, F]
+    const float2* s;     // maps [N, N, C]
+    const float* mask;   // [N, N] or null
+    float2* z;           // scratch [N, N, C, F]
+    float2* out;         // [N, N, F]
+    const float2* tw_fwd;
+    const float2* tw_inv;
+    std::uint32_t coils;
+    std::uint32_t frames;
+    int shift;
+    float scale;         // 1 / (N * N)
+    int phases = 7;      // timing experiments only (HETRECO_NORMAL_PHASES): bit i runs phase i
+};
+LaunchShape plan_sense_normal_fused(std::uint64_t N, std::uint64_t planes, int device_sms);
+cudaError_t launch_sense_normal_fused(std::uint64_t N, const SenseNormalArgs& a, const LaunchShape& s,
+                                      cudaStream_t stream);
+
 // ---- axis-0 + combine fed by a TMA bulk-copy ring (fft_combine_tma.cu) -----------
 // Same contract as launch_contig with mode Sense/Rss and fp32 accumulation;
 // a.in = X [N, ny, C, F].  HETRECO_TMA_STAGES (2|3|4|6, default 4) = tiles in

@@ -123,3 +123,17 @@ def test_sense_forward_rectangular(s, nx, ny):
         run(s, "sense_forward", [M, S, np.ones((nx, ny), np.float32)], (nx, ny, 3, 2))
     with pytest.raises(h.ShapeMismatch):
         run(s, "sense_normal", [M, S], (nx, ny, 2))
+
+
+@pytest.mark.parametrize("n,nc,nf,points", [(256, 8, 1, "8"), (256, 8, 2, "16"), (64, 3, 2, "8"), (128, 5, 1, "16")])
+def test_sense_normal_fused_cooperative(s, monkeypatch, n, nc, nf, points):
+    """The opt-in single cooperative kernel (fft_sense_normal.cu, measured
+    slower than the three-kernel graph: profiles/round2_c4.md) stays exact."""
+    monkeypatch.setenv("HETRECO_NORMAL_FUSED", "1")
+    monkeypatch.setenv("HETRECO_NORMAL_POINTS", points)
+    rng = np.random.default_rng(3 * n + nc)
+    M = cplx(rng, n, n, nf)
+    S = cplx(rng, n, n, nc)
+    mask = np.asfortranarray((rng.random((n, n)) < 0.4).astype(np.float32))
+    out, *_ = run(s, "sense_normal", [M, S, mask], (n, n, nf))
+    assert relmax(out, o.sense_normal(M, S, mask)) <= TOL
