@@ -1,4 +1,9 @@
 // fft_strided.cu -- host plan/launch for the axis-1 (strided) pass.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <mutex>
+
 #include "fft_kernels.cuh"
 
 namespace hetreco::dev {
@@ -81,6 +86,139 @@ __global__ void __launch_bounds__(TX * (N / RQ)) k_fft_strided_ring(StridedArgs 
     cp_async_wait<0>();
 }
 
+// ---- the same column-tile ring fed by TMA (cp.async.bulk.tensor.2d) ------------------
+//
+// one elected thread issues the tile as 2-D tensor-map boxes
+// ([TX columns x <=256 rows] of the [planes*N rows, N] view; two boxes at
+// 512 rows) completing on the stage's mbarrier, instead of 1024 threads
+// issuing 16-byte cp.async chunks.  Shared-memory layout, consumer reads,
+// transform and stores are those of k_fft_strided_ring (bit-identical).
+// The stage a TMA refills was last read before the previous iteration's
+// transform, whose block barriers every thread has passed -- no extra barrier.
+__device__ __forceinline__ std::uint32_t smem_addr(const void* p) {
+    return static_cast<std::uint32_t>(__cvta_generic_to_shared(p));
+}
+
+template <int N, int DIR, int RQ, int K, int TX>
+__global__ void __launch_bounds__(TX * (N / RQ)) k_fft_strided_tma(const __grid_constant__ CUtensorMap map,
+                                                                   StridedArgs a, std::uint32_t ntiles) {
+    pdl_launch_dependents();
+    using L = LineFFT<N, RQ>;
+    constexpr int R = L::R, T = L::T;
+    constexpr int TILE = N * TX;  // float2 per stage
+    constexpr int BOX_ROWS = N < 256 ? N : 256;
+    constexpr std::uint32_t STAGE_BYTES = std::uint32_t(TILE) * 8;
+    extern __shared__ __align__(128) float2 smem[];
+    const int tid = threadIdx.x;
+    const int l = tid % TX, j = tid / TX;
+    float2* ring = smem;
+    float2* line = smem + K * TILE + l * line_stride<N>();
+    std::uint64_t* full = reinterpret_cast<std::uint64_t*>(smem + K * TILE + TX * line_stride<N>());
+    typename L::Twiddles tw;
+    L::load_twiddles(tw, a.tw, j, a.scale);
+    if (tid == 0) {
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<std::uint64_t>(&map)) : "memory");
+        for (int k = 0; k < K; ++k)
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(full + k)) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    pdl_wait();  // the input is the previous kernel's output
+    constexpr std::uint32_t xtiles = N / TX;
+    const bool sh_in = a.shift_in, sh_out = a.shift_out;
+    auto issue = [&](std::uint32_t tile, int stage) {  // thread 0 only
+        if (tile >= ntiles) return;
+        const std::uint32_t plane = tile / xtiles, xt = tile % xtiles;
+        const std::uint32_t bar = smem_addr(full + stage);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(STAGE_BYTES) : "memory");
+        for (int b = 0; b < N / BOX_ROWS; ++b) {
+            const std::uint32_t dst = smem_addr(ring + stage * TILE + b * BOX_ROWS * TX);
+            const int c0 = int(xt) * 2 * TX, c1 = int(plane) * N + b * BOX_ROWS;
+            asm volatile(
+                "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
+                "[%4];" ::"r"(dst),
+                "l"(reinterpret_cast<std::uint64_t>(&map)), "r"(c0), "r"(c1), "r"(bar)
+                : "memory");
+        }
+    };
+    std::uint32_t tile = blockIdx.x;
+    if (tid == 0)
+        for (int k = 0; k < K - 1; ++k) issue(tile + std::uint32_t(k) * gridDim.x, k);
+    for (int i = 0; tile < ntiles; ++i, tile += gridDim.x) {
+        const int stage = i % K;
+        const std::uint32_t parity = std::uint32_t(i / K) & 1u;
+        std::uint32_t ok = 0;
+        do {
+            asm volatile(
+                "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+                : "=r"(ok)
+                : "r"(smem_addr(full + stage)), "r"(parity)
+                : "memory");
+        } while (!ok);
+        if (tid == 0) issue(tile + std::uint32_t(K - 1) * gridDim.x, (i + K - 1) % K);
+        const float2* t = ring + stage * TILE + l;
+        float2 v[R];
+        slots_ld<R>(sh_in, (long long)(R / 2) * T,
+                    [&](auto m, long long d) { v[m.value] = t[(j + T * m.value + int(d)) * TX]; });
+        L::template run<DIR>(v, tw, line, j, [] { __syncthreads(); }, a.scale);
+        float2* dst = a.out + std::uint64_t(tile / xtiles) * N * N + (tile % xtiles) * TX + l + std::uint32_t(j) * N;
+        slots<R>(sh_out, [&](auto m, auto ms) { dst[ms.value * T * N] = v[m.value]; });
+    }
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 strided_map_encoder() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        cudaDriverEntryPointQueryResult q{};
+        void* p = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+        else
+            cudaGetLastError();
+    });
+    return fn;
+}
+
+template <int N, int RQ, int K, int TX>
+cudaError_t tma_ring_launch(int dir, const StridedArgs& a, const LaunchShape& s, std::uint32_t tiles, cudaStream_t st) {
+    auto enc = strided_map_encoder();
+    if (!enc) return cudaErrorNotSupported;
+    CUtensorMap map;
+    cuuint64_t dims[2] = {cuuint64_t(2 * N), cuuint64_t(a.planes) * N};  // float32 elements, rows
+    cuuint64_t strides[1] = {cuuint64_t(N) * 8};
+    cuuint32_t box[2] = {cuuint32_t(2 * TX), cuuint32_t(N < 256 ? N : 256)};
+    cuuint32_t estr[2] = {1, 1};
+    if (enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float2*>(a.in), dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        return cudaErrorInvalidValue;
+    if (dir > 0)
+        k_fft_strided_tma<N, 1, RQ, K, TX><<<s.grid, s.block, s.smem, st>>>(map, a, tiles);
+    else
+        k_fft_strided_tma<N, -1, RQ, K, TX><<<s.grid, s.block, s.smem, st>>>(map, a, tiles);
+    return cudaGetLastError();
+}
+
+template <int N, int RQ, int K, int TX>
+int tma_ring_smem() {
+    return (K * N * TX + TX * line_stride<N>()) * 8 + K * 8;
+}
+
+template <int N, int RQ, int K, int TX>
+int tma_ring_occ(int block, int smem) {
+    return std::max(blocks_per_sm(k_fft_strided_tma<N, 1, RQ, K, TX>, block, smem),
+                    blocks_per_sm(k_fft_strided_tma<N, -1, RQ, K, TX>, block, smem));
+}
+
+// TMA boxes instead of cp.async chunks (profiles/round2_tma_axis1.md): the
+// default at 512^2 (axis-1 184 -> 170 us at 512^2 x 32 coils x 8 frames, ncu
+// 185 -> 166 us, same DRAM bytes); at 256^2 the cp.async ring stays (162 vs
+// 165 us).  HETRECO_STRIDED_TMA=0|1 forces it off / on at both sizes.
+bool tma_ring_enabled(std::uint64_t N) { return env_int("HETRECO_STRIDED_TMA", N == 512 ? 1 : 0) == 1; }
+
 // Stages K and columns per tile.  Measured (profiles/round1_summary.md),
 // axis-1 us at 512^2 x 32 coils x 8 frames: register prefetch 260; 8 columns
 // with K = 3/4/5 stages 252/240/240; 16 columns (128-byte row segments,
@@ -154,18 +292,28 @@ int strided_occ(int block, int smem, int variant) {
 }
 
 template <int N, int RQ>
-void strided_go(int dir, bool sq, const StridedArgs& a, const LaunchShape& s, int tx, std::uint32_t tiles,
+cudaError_t strided_go(int dir, bool sq, const StridedArgs& a, const LaunchShape& s, int tx, std::uint32_t tiles,
                 cudaStream_t st) {
+    if constexpr (N == 512 && RQ == 8) {
+        if (sq && (s.variant & 64)) {
+            return tma_ring_launch<512, 8, 2, 16>(dir, a, s, tiles, st);
+        }
+    }
+    if constexpr (N == 256 && RQ == 16) {
+        if (sq && (s.variant & 64)) {
+            return tma_ring_launch<256, 16, 2, 32>(dir, a, s, tiles, st);
+        }
+    }
     if constexpr (N == 512 && RQ == 8) {
         if (sq && (s.variant & 4)) {
             ring_go<N, RQ>(dir, (s.variant >> 3) & 7, tx, a, s, tiles, st);
-            return;
+            return cudaSuccess;
         }
     }
     if constexpr (N == 256 && RQ == 16) {
         if (sq && (s.variant & 4)) {
             ring_launch<N, RQ, 2, 32>(dir, a, s, tiles, st);
-            return;
+            return cudaSuccess;
         }
     }
     if constexpr (has_variants<N>()) {
@@ -174,14 +322,14 @@ void strided_go(int dir, bool sq, const StridedArgs& a, const LaunchShape& s, in
                 k_fft_strided<N, 1, N, RQ, false, 3><<<s.grid, s.block, s.smem, st>>>(a, tx, tiles);
             else
                 k_fft_strided<N, -1, N, RQ, false, 3><<<s.grid, s.block, s.smem, st>>>(a, tx, tiles);
-            return;
+            return cudaSuccess;
         }
         if (sq && (s.variant & 1)) {  // register prefetch of the next tile (square fast path)
             if (dir > 0)
                 k_fft_strided<N, 1, N, RQ, true><<<s.grid, s.block, s.smem, st>>>(a, tx, tiles);
             else
                 k_fft_strided<N, -1, N, RQ, true><<<s.grid, s.block, s.smem, st>>>(a, tx, tiles);
-            return;
+            return cudaSuccess;
         }
     }
     if (dir > 0) {
@@ -195,6 +343,7 @@ void strided_go(int dir, bool sq, const StridedArgs& a, const LaunchShape& s, in
         else
             k_fft_strided<N, -1, 0, RQ><<<s.grid, s.block, s.smem, st>>>(a, tx, tiles);
     }
+    return cudaSuccess;
 }
 
 }  // namespace
@@ -239,6 +388,22 @@ LaunchShape plan_strided(std::uint64_t N, std::uint64_t nx, std::uint64_t planes
     s.smem = int(tx) * ls_bytes;
     const std::uint64_t tiles = (nx / tx) * planes;
     int occ = 1;
+    if (N == 256 && R == 16 && nx == 256 && ring_stages() && !few_tiles && tma_ring_enabled(256)) {
+        s.variant = 64 | (2 << 3);
+        s.block = 32 * T;
+        s.smem = tma_ring_smem<256, 16, 2, 32>();
+        occ = tma_ring_occ<256, 16, 2, 32>(s.block, s.smem);
+        s.grid = int(std::min<std::uint64_t>((nx / 32) * planes, std::uint64_t(sms) * occ));
+        return s;
+    }
+    if (N == 512 && R == 8 && nx == 512 && ring_stages() && !few_tiles && tma_ring_enabled(512)) {
+        s.variant = 64 | (2 << 3);
+        s.block = 16 * T;
+        s.smem = tma_ring_smem<512, 8, 2, 16>();
+        occ = tma_ring_occ<512, 8, 2, 16>(s.block, s.smem);
+        s.grid = int(std::min<std::uint64_t>((nx / 16) * planes, std::uint64_t(sms) * occ));
+        return s;
+    }
     if (N == 256 && R == 16 && nx == 256 && ring_stages() && !few_tiles) {  // 32 columns (256-B rows), 2 stages
         s.variant = 4 | (2 << 3);
         s.block = 32 * T;
@@ -289,10 +454,10 @@ cudaError_t launch_strided(std::uint64_t N, int dir, const StridedArgs& a, const
     case n:                                                               \
         if constexpr (has_variants<n>())                                  \
             if (s.rq == 8 && LineFFT<n>::R != 8) {                        \
-                strided_go<n, 8>(dir, sq, a, s, tx, tiles, st);           \
+                if (auto e = strided_go<n, 8>(dir, sq, a, s, tx, tiles, st)) return e; \
                 break;                                                    \
             }                                                             \
-        strided_go<n, default_points(n)>(dir, sq, a, s, tx, tiles, st);   \
+        if (auto e = strided_go<n, default_points(n)>(dir, sq, a, s, tx, tiles, st)) return e; \
         break;
         HETRECO_FFT_SIZES(X)
 #undef X

@@ -665,6 +665,28 @@ def test_strided_ring(s, monkeypatch, n, stages, shift):
         assert beq(a, b)
 
 
+@pytest.mark.parametrize("n,planes", [(256, (3, 5)), (512, (2, 3)), (256, (32, 2))])
+@pytest.mark.parametrize("shift", [False, True])
+def test_strided_tma_ring(s, monkeypatch, n, planes, shift):
+    """The axis-1 column-tile ring fed by TMA boxes (k_fft_strided_tma,
+    HETRECO_STRIDED_TMA=1) gives the same bits as the cp.async ring for the
+    SENSE chain and fft2d in both directions."""
+    nc, nf = planes
+    rng = np.random.default_rng(n + nc)
+    Y = cplx(rng, n, n, nc, nf)
+    S = cplx(rng, n, n, nc)
+    outs = {}
+    for tma in ("0", "1"):
+        monkeypatch.setenv("HETRECO_STRIDED_TMA", tma)
+        (M,), _ = run_process(s, "sens_recon", [Y, S], [((n, n, nf), np.complex64)], {"shift": shift})
+        x = np.asfortranarray(Y[:, :, :, 0])
+        (fw,), _ = run_process(s, "fft2d", [x], [(x.shape, np.complex64)], {"direction": "forward", "shift": shift})
+        (bw,), _ = run_process(s, "fft2d", [x], [(x.shape, np.complex64)], {"direction": "inverse", "shift": shift})
+        outs[tma] = (M, fw, bw)
+    for a, b in zip(outs["0"], outs["1"]):
+        assert beq(a, b)
+
+
 @pytest.mark.parametrize("method", ["sens_recon", "rss_recon"])
 def test_recon_overlap_pipeline_bitexact(s, method):
     """"overlap": true -- chunked axis-1/combine graph branches (fork/join over a
