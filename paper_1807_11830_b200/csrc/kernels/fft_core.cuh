@@ -113,6 +113,36 @@ __device__ __forceinline__ float2 wmul(float2 v) {
     }
 }
 
+// Radix-2 butterfly with a compile-time twiddle: (u, b) <- (u + W b, u - W b),
+// W = W_N^K (N | 64).  Trivial twiddles (+-1, +-i) cost 4 FADD.  Others use
+// the factored form W b = c (b.x - t b.y, b.y + t b.x) with |t| <= 1 (t = s/c,
+// or the roles of c and s swapped when |s| > |c|): 2 FFMA for the bracket and
+// 4 FFMA for u +- c (.), i.e. 6 FP32 instructions instead of 4 (W b) + 4 (u +- .).
+template <int N, int K, int DIR>
+__device__ __forceinline__ void bfly_tw(float2& u, float2& b) {
+    constexpr int k = ((K % N) + N) % N;
+    if constexpr (k == 0 || 2 * k == N || 4 * k == N || 4 * k == 3 * N) {
+        const float2 t = wmul<N, K, DIR>(b);
+        const float2 x = u;
+        u = cadd(x, t);
+        b = csub(x, t);
+    } else {
+        constexpr int idx = k * (64 / N);
+        constexpr double c = cos64(idx), s = DIR * sin64(idx);
+        constexpr bool cos_major = (c < 0 ? -c : c) >= (s < 0 ? -s : s);
+        constexpr float f = float(cos_major ? c : s);        // common factor
+        constexpr float t = float(cos_major ? s / c : c / s);  // |t| <= 1
+        float2 r;
+        if constexpr (cos_major)  // W b = c (b.x - t b.y, b.y + t b.x)
+            r = make_float2(fmaf(-t, b.y, b.x), fmaf(t, b.x, b.y));
+        else                      // W b = s (t b.x - b.y, t b.y + b.x)
+            r = make_float2(fmaf(t, b.x, -b.y), fmaf(t, b.y, b.x));
+        const float2 x = u;
+        u = make_float2(fmaf(f, r.x, x.x), fmaf(f, r.y, x.y));
+        b = make_float2(fmaf(-f, r.x, x.x), fmaf(-f, r.y, x.y));
+    }
+}
+
 // i * DIR * v  (multiplication by +-i)
 template <int DIR>
 __device__ __forceinline__ float2 mul_i(float2 v) {
@@ -160,10 +190,7 @@ __device__ __forceinline__ void dft_regs(float2 (&v)[R]) {
             sfor<Rp / m>([&](auto b) {
                 sfor<h>([&](auto kk) {
                     constexpr int i0 = b.value * m + kk.value;
-                    const float2 t = wmul<m, kk.value, DIR>(a[i0 + h]);
-                    const float2 u = a[i0];
-                    a[i0] = cadd(u, t);
-                    a[i0 + h] = csub(u, t);
+                    bfly_tw<m, kk.value, DIR>(a[i0], a[i0 + h]);
                 });
             });
         });
