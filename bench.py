@@ -306,6 +306,21 @@ def run_ours(args):
     device_resident = {"value": NF * dev_steps / t_dev_max, "unit": UNIT, "steps": dev_steps,
                        "ms_per_step": t_dev_max / dev_steps * 1e3,
                        "note": "sens_recon process over the rank's slab resident in HBM (no host transfers)"}
+    # the reference's rounding (fp32 products, fp64 coil-ordered sums, ximage_sum.cl.src:6-23) timed too
+    p64 = h.Process(s, "sens_recon").set_input(hin).set_output(hout).init({"accumulate": "fp64"})
+    for _ in range(max(args.warmup, 3)):
+        p64.launch()
+    s.synchronize()
+    barrier(world)
+    s.timer_start()
+    for _ in range(20):
+        p64.launch()
+    t64 = reduce_max(s.timer_stop(), world)
+    barrier(world)
+    device_resident["fp64_accumulate"] = {"value": NF * 20 / t64, "unit": UNIT, "ms_per_step": t64 / 20 * 1e3,
+                                          "note": "same chain with accumulate=fp64 (the reference combine's "
+                                                  "rounding; bit-exact combine given the same X)"}
+    del p64
 
     # per-kernel device times (events between kernels on the compute stream)
     prof = p.profile(reps=10)  # [axis1, combine] per frame chunk (one chunk by default)
