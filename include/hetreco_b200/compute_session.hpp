@@ -92,7 +92,10 @@ private:
         DataKind kind = DataKind::Generic;
     };
     const Entry& resolve(DataHandle handle) const;
-    DataHandle insert(const LayoutDescriptor& layout, DataKind kind, const std::vector<const void*>* payload);
+    // record `index` of a live entry, with `role` naming the side in errors
+    const LayoutRecord& record_of(const Entry& e, std::size_t index, const char* role) const;
+    DataHandle insert(const LayoutDescriptor& layout, DataKind kind, std::span<const void* const> payload);
+    void drop_buffers(const Entry& e) noexcept;
 
     Backend& backend_;
     DeviceDescriptor device_;
