@@ -152,6 +152,9 @@ protected:
     void mark(cudaStream_t s);
     // true while profile() replays record() kernel by kernel (no graph)
     bool profiling() const { return profiling_; }
+    // Whether the captured graph's kernel -> kernel edges become programmatic
+    // (PDL) edges.  Per-process measured default (HETRECO_PDL=0|1 overrides).
+    virtual bool programmatic_edges() const { return false; }
 
 private:
     void snapshot_layouts();

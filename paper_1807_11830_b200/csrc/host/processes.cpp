@@ -387,24 +387,26 @@ void GraphProcess::on_rebind() {
 
 namespace {
 
-// Programmatic dependent launch inside process graphs (HETRECO_PDL=1, opt-in):
-// every kernel -> kernel edge of a captured graph becomes a programmatic edge
-// (kernels/pdl.cuh: the upstream kernel triggers at entry, the downstream one
-// waits before it touches data), so the launch of kernel i+1 and its prologue
-// overlap the tail of kernel i.  Measured on B200 (profiles/round2_small_
-// configs.md): no gain on the small configs (C2 8.47 -> 8.46 us, C4 12.75 ->
-// 12.56 us) and C3 slower (266 -> 329 us), so full-completion edges stay the
-// default.
-bool pdl_enabled() {
-    static const bool on = [] {
-        const char* v = std::getenv("HETRECO_PDL");
-        return v && *v == '1';
+// Programmatic dependent launch inside process graphs: every kernel ->
+// kernel edge of a captured graph becomes a programmatic edge (kernels/pdl.cuh:
+// the upstream kernel triggers at entry, the downstream one waits before it
+// touches data), so the launch of kernel i+1 and its prologue overlap the tail
+// of kernel i.  Measured on B200 (profiles/round2_small_configs.md): C4 (the
+// three-kernel normal operator) 12.76 -> 12.56 us, C2 unchanged, C3 263 ->
+// 324 us (early-launched combine CTAs hold SM slots through the axis-1 tail).
+// So it is on only where it wins (GraphProcess::programmatic_edges(): the
+// SENSE model processes); HETRECO_PDL=1 / 0 forces it on / off everywhere.
+int pdl_override() {
+    static const int v = [] {
+        const char* e = std::getenv("HETRECO_PDL");
+        return (e && *e == '1') ? 1 : (e && *e == '0') ? 0 : -1;
     }();
-    return on;
+    return v;
 }
 
-void make_kernel_edges_programmatic(cudaGraph_t g) {
-    if (!pdl_enabled()) return;
+void make_kernel_edges_programmatic(cudaGraph_t g, bool wanted) {
+    const int o = pdl_override();
+    if (!(o == 1 || (o < 0 && wanted))) return;
     size_t n = 0;
     if (cudaGraphGetEdges_v2(g, nullptr, nullptr, nullptr, &n) != cudaSuccess || n == 0) {
         cudaGetLastError();
@@ -450,7 +452,7 @@ void GraphProcess::capture(bool update) {
     cudaStreamDestroy(cs);
     ck(e, "capture of process '" + name() + "'");
     try {
-        make_kernel_edges_programmatic(g);
+        make_kernel_edges_programmatic(g, programmatic_edges());
     } catch (...) {
         cudaGraphDestroy(g);
         throw;
@@ -1187,6 +1189,8 @@ public:
                                                     : dev::plan_contig(nx_, dev::Combine::Sense, ny_ * nf_, sms);
         }
     }
+    // chain of 2-3 small dependent kernels: PDL edges measured faster (C4)
+    bool programmatic_edges() const override { return true; }
     void repoint() override {
         m_ = static_cast<const float2*>(session().device_array(require_input(), 0));
         s_ = static_cast<const float2*>(session().device_array(require_input(), 1));

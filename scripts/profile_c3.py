@@ -4,6 +4,7 @@ Used under ncu (kernel captures) and for variant sweeps:
     HETRECO_COMBINE_VARIANT=1 HETRECO_CHUNK=2 python scripts/profile_c3.py --reps 20
 """
 import argparse
+import json
 import os
 import sys
 
@@ -20,6 +21,7 @@ ap.add_argument("--frames", type=int, default=30)
 ap.add_argument("--launches", type=int, default=3)
 ap.add_argument("--reps", type=int, default=10)
 ap.add_argument("--timed", type=int, default=50, help="graph launches timed back to back")
+ap.add_argument("--params", default="{}", help="process params as JSON, e.g. '{\"overlap\": true}'")
 a = ap.parse_args()
 nx = ny = a.nx
 rng = np.random.default_rng(0)
@@ -33,7 +35,7 @@ if a.method == "sens_recon":
 else:
     hin = s.register_data(h.Data([Y], h.DataKind.KData))
     hout = s.allocate_data([((nx, ny, a.frames), np.float32)])
-p = h.Process(s, a.method).set_input(hin).set_output(hout).init()
+p = h.Process(s, a.method).set_input(hin).set_output(hout).init(json.loads(a.params))
 for _ in range(a.launches):
     p.launch()
 s.synchronize()
@@ -52,3 +54,9 @@ if a.reps:
           f"chunk={os.environ.get('HETRECO_CHUNK', 'auto')} kernels={len(t)} | axis1 {t1*1e6:.1f} us {b1/t1/1e9:.0f} GB/s "
           f"| axis0+combine {t2*1e6:.1f} us {b2/max(t2, 1e-12)/1e9:.0f} GB/s | sum {(t1+t2)*1e6:.1f} us | graph {tg*1e6:.1f} us "
           f"= {a.frames/tg:.0f} frames/s")
+else:
+    s.timer_start()
+    for _ in range(a.timed):
+        p.launch()
+    tg = s.timer_stop() / a.timed
+    print(f"{a.method} {nx}x{ny}x{a.coils}x{a.frames} params={a.params} graph {tg*1e6:.1f} us = {a.frames/tg:.0f} frames/s")
