@@ -54,7 +54,7 @@ if a.reps:
           f"chunk={os.environ.get('HETRECO_CHUNK', 'auto')} kernels={len(t)} | axis1 {t1*1e6:.1f} us {b1/t1/1e9:.0f} GB/s "
           f"| axis0+combine {t2*1e6:.1f} us {b2/max(t2, 1e-12)/1e9:.0f} GB/s | sum {(t1+t2)*1e6:.1f} us | graph {tg*1e6:.1f} us "
           f"= {a.frames/tg:.0f} frames/s")
-else:
+elif a.timed:
     s.timer_start()
     for _ in range(a.timed):
         p.launch()
