@@ -502,8 +502,10 @@ def c5_stream(h, s, rank: int, world: int, total_frames: int, sampler):
 
 
 def _device_time(s, fn, reps: int) -> float:
-    """Mean device seconds of fn() over reps (CUDA events on the compute stream)."""
-    for _ in range(3):
+    """Mean device seconds of fn() over reps (CUDA events on the compute stream),
+    after 50 untimed calls (the latency-bound configs are host-issue bound, so
+    the host side is warmed too)."""
+    for _ in range(50):
         fn()
     s.synchronize()
     s.timer_start()
@@ -522,21 +524,22 @@ def other_configs(h, s, peak: float):
     hx = s.register_data([x])
     hy = s.allocate_data([((512, 512), np.float32)])
     p = h.Process(s, "negate").set_input(hx).set_output(hy).init({"max_value": 1.0})  # LaunchStats sampled
-    t = _device_time(s, p.launch, 200)
+    t = _device_time(s, p.launch, 1000)
     # the same loop with every launch timed (two CUDA event records per launch)
     ps = h.Process(s, "negate").set_input(hx).set_output(hy).init({"max_value": 1.0, "launch_timing": "every"})
-    ts = _device_time(s, ps.launch, 200)
+    ts = _device_time(s, ps.launch, 1000)
     out["C1_negate_512x512_f32"] = {"us_per_image": t * 1e6, "images_per_s": 1 / t,
                                     "gbs": 2 * x.nbytes / t / 1e9, "frac_of_hbm": 2 * x.nbytes / t / 1e9 / peak,
                                     "us_per_image_every_launch_timed": ts * 1e6,
-                                    "note": "2 MB per image: launch-latency bound (one graph launch per image)"}
+                                    "note": "2 MB per image: host-issue bound (one Python -> C-ABI -> cudaGraphLaunch per image; "
+                                            "device time per launch = host time per launch, profiles/round2_small_configs.md)"}
     # C2: single-frame 256x256, 8 coils, IFFT + RSS
     Y2 = np.asfortranarray((rng.standard_normal((256, 256, 8, 1), dtype=np.float32)
                             + 1j * rng.standard_normal((256, 256, 8, 1), dtype=np.float32)).astype(np.complex64))
     hk = s.register_data(h.Data([Y2], h.DataKind.KData))
     hr = s.allocate_data([((256, 256, 1), np.float32)], h.DataKind.XData)
     p2 = h.Process(s, "rss_recon").set_input(hk).set_output(hr).init()
-    t2 = _device_time(s, p2.launch, 200)
+    t2 = _device_time(s, p2.launch, 1000)
     out["C2_rss_256x256x8x1"] = {"us_per_frame": t2 * 1e6, "frames_per_s": 1 / t2,
                                  "gbs": (Y2.nbytes + 256 * 256 * 4) / t2 / 1e9}
     # C4: iterative loop -- normal operator E^H E (FFT + mask + IFFT + coil combine)
@@ -568,7 +571,8 @@ def other_configs(h, s, peak: float):
         "kernel_us_unlinked": [round(x * 1e6, 2) for x in prof4],
         "kernels_per_launch": len(prof4),
         "note": "one cudaGraphLaunch per launch(); plans/twiddles baked in init(); kernels linked by "
-                "programmatic (PDL) edges; kernel_us_unlinked = per-kernel times without the graph"}
+                "programmatic (PDL) graph edges (this process' default); kernel_us_unlinked = per-kernel "
+                "times without the graph"}
     return out
 
 
