@@ -23,12 +23,39 @@ namespace {
 // 2: 159 (register-prefetch kernel 162).  HETRECO_SS_LINES = 2|4|8|16 overrides.
 constexpr int kSsLines = 8;
 
+__device__ __forceinline__ std::uint32_t smem_u32addr(const void* p) {
+    return static_cast<std::uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ float2 lds_f2(std::uint32_t addr) {
+    float2 v;
+    asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(addr));
+    return v;
+}
+
+// Pass twiddles from shared memory (TWS) at 256 points: A/B switch
+// HETRECO_SS_TWSMEM=0|1 (profiles/round2_summary.md).
+bool ss_tws(std::uint64_t N) { return N == 256 && env_int("HETRECO_SS_TWSMEM", 0) == 1; }
+
 int ss_lines(std::uint64_t N) {
     const int v = env_int("HETRECO_SS_LINES", N >= 512 ? 2 : 4);
     return (v == 2 || v == 4 || v == 6 || v == 8 || v == 16) ? v : kSsLines;
 }
 
-template <int N, int LPB>
+// TWS (two-pass lengths, 256 = 16 x 16): the pass-1 twiddles W^{j q} (x
+// scale, q = 1..15) come from a per-CTA shared table laid out [j][q - 1] --
+// row stride 15 float2, so the 16 threads of a line hit 16 distinct bank
+// pairs -- read at the point of use, instead of 30 registers per thread.
+template <int N>
+constexpr bool tws_ok() {
+    using L = LineFFT<N>;
+    return L::P == 2 && !L::kTableTw && L::R == L::radix(1) && L::R == L::T;
+}
+template <int N>
+constexpr int tws_len() {
+    return tws_ok<N>() ? LineFFT<N>::T * (LineFFT<N>::R - 1) : 0;
+}
+
+template <int N, int LPB, bool TWS>
 __global__ void __launch_bounds__(LPB * LineFFT<N>::T) k_fft_combine_ss(ContigArgs a, std::uint32_t gpy,
                                                                         std::uint32_t groups) {
     pdl_launch_dependents();
@@ -37,11 +64,22 @@ __global__ void __launch_bounds__(LPB * LineFFT<N>::T) k_fft_combine_ss(ContigAr
     constexpr int NS = (N + NT - 1) / NT;  // map elements staged per thread
     extern __shared__ float2 smem[];
     float2* sbuf = smem + LPB * line_stride<N>();  // 2 x [N]
+    float2* twt = sbuf + 2 * N;                    // TWS: [T][R - 1]
     const int tid = threadIdx.x;
     const int j = tid % T, l = tid / T;
     float2* line = smem + l * line_stride<N>();
     typename L::Twiddles tw;
-    L::load_twiddles(tw, a.tw, j, a.scale);
+    if constexpr (TWS) {
+        static_assert(tws_ok<N>(), "shared pass twiddles need a 2-pass plan with R = T");
+        for (int i = tid; i < tws_len<N>(); i += NT) {
+            const int jj = i / (R - 1), q = i % (R - 1) + 1;
+            const float2 w = __ldg(a.tw + L::template tw_index<1, 0, 0>(jj) * q);
+            twt[i] = make_float2(w.x * a.scale, w.y * a.scale);
+        }
+    } else {
+        L::load_twiddles(tw, a.tw, j, a.scale);
+    }
+    const std::uint32_t tws_row = smem_u32addr(twt + j * (R - 1));
     pdl_wait();  // twiddle tables are init-time constants
     const bool sh_in = a.shift_in, sh_out = a.shift_out;
     const std::uint32_t C = std::uint32_t(a.coils), ny = std::uint32_t(a.ny), F = std::uint32_t(a.frames);
@@ -89,7 +127,14 @@ __global__ void __launch_bounds__(LPB * LineFFT<N>::T) k_fft_combine_ss(ContigAr
                 load_x(c + 1, xn);
                 load_s(c + 1);
             }
-            L::template run<+1>(v, tw, line, j, [] { line_sync<T>(); }, a.scale);
+            if constexpr (TWS) {
+                // volatile shared loads: re-read per coil, never hoisted into registers
+                L::template run_f<+1>(
+                    v, [&](auto, auto, auto qc) { return lds_f2(tws_row + 8u * qc.value); }, line, j,
+                    [] { line_sync<T>(); }, a.scale);
+            } else {
+                L::template run<+1>(v, tw, line, j, [] { line_sync<T>(); }, a.scale);
+            }
             const float2* sb = sbuf + (c & 1) * N + j;
             slots_ld<R>(sh_out, (long long)(R / 2) * T, [&](auto m, long long o) {
                 mac_conj(acc_re[m.value], acc_im[m.value], v[m.value], sb[T * m.value + o]);
@@ -104,25 +149,31 @@ __global__ void __launch_bounds__(LPB * LineFFT<N>::T) k_fft_combine_ss(ContigAr
     }
 }
 
-template <int N, int LPB>
+template <int N, int LPB, bool TWS>
 constexpr int ss_smem() {
-    return (LPB * line_stride<N>() + 2 * N) * 8;
+    return (LPB * line_stride<N>() + 2 * N + (TWS ? tws_len<N>() : 0)) * 8;
+}
+
+template <int n, int LPB, bool TWS>
+LaunchShape plan_ss_nlt(std::uint64_t ny, std::uint64_t frames, int sms) {
+    LaunchShape s;
+    if constexpr (n >= 64 && LPB * LineFFT<n>::T <= 1024 && (!TWS || tws_ok<n>())) {
+        s.rq = LineFFT<n>::R;
+        s.block = LPB * LineFFT<n>::T;
+        s.smem = ss_smem<n, LPB, TWS>();
+        const std::uint64_t groups = ny * ((frames + LPB - 1) / LPB);
+        const int occ = blocks_per_sm(k_fft_combine_ss<n, LPB, TWS>, s.block, s.smem);
+        const int per_sm = env_int("HETRECO_SS_CTAS_PER_SM", occ);  // experiments (profiles/round1_combine.md)
+        s.grid = int(std::min<std::uint64_t>(groups, std::uint64_t(sms) * std::uint64_t(per_sm > 0 ? per_sm : occ)));
+        s.variant = 256 | (LPB << 10) | (TWS ? (1 << 15) : 0);
+    }
+    return s;
 }
 
 template <int n, int LPB>
 LaunchShape plan_ss_nl(std::uint64_t ny, std::uint64_t frames, int sms) {
-    LaunchShape s;
-    if constexpr (n >= 64 && LPB * LineFFT<n>::T <= 1024) {
-        s.rq = LineFFT<n>::R;
-        s.block = LPB * LineFFT<n>::T;
-        s.smem = ss_smem<n, LPB>();
-        const std::uint64_t groups = ny * ((frames + LPB - 1) / LPB);
-        const int occ = blocks_per_sm(k_fft_combine_ss<n, LPB>, s.block, s.smem);
-        const int per_sm = env_int("HETRECO_SS_CTAS_PER_SM", occ);  // experiments (profiles/round1_combine.md)
-        s.grid = int(std::min<std::uint64_t>(groups, std::uint64_t(sms) * std::uint64_t(per_sm > 0 ? per_sm : occ)));
-        s.variant = 256 | (LPB << 10);
-    }
-    return s;
+    if (ss_tws(n)) return plan_ss_nlt<n, LPB, true>(ny, frames, sms);
+    return plan_ss_nlt<n, LPB, false>(ny, frames, sms);
 }
 
 template <int n>
@@ -136,22 +187,27 @@ LaunchShape plan_ss_n(std::uint64_t ny, std::uint64_t frames, int sms) {
     }
 }
 
-template <int n, int LPB>
-cudaError_t launch_ss_nl(const ContigArgs& a, const LaunchShape& s, cudaStream_t st) {
-    if constexpr (n >= 64 && LPB * LineFFT<n>::T <= 1024) {
+template <int n, int LPB, bool TWS>
+cudaError_t launch_ss_nlt(const ContigArgs& a, const LaunchShape& s, cudaStream_t st) {
+    if constexpr (n >= 64 && LPB * LineFFT<n>::T <= 1024 && (!TWS || tws_ok<n>())) {
         const std::uint64_t gpy = (a.frames + LPB - 1) / LPB;
         const std::uint64_t groups = a.ny * gpy;
         if (groups >= (std::uint64_t(1) << 32)) return cudaErrorInvalidValue;
-        k_fft_combine_ss<n, LPB><<<s.grid, s.block, s.smem, st>>>(a, std::uint32_t(gpy), std::uint32_t(groups));
+        k_fft_combine_ss<n, LPB, TWS><<<s.grid, s.block, s.smem, st>>>(a, std::uint32_t(gpy), std::uint32_t(groups));
         return cudaGetLastError();
     } else {
         return cudaErrorInvalidValue;
     }
 }
 
+template <int n, int LPB>
+cudaError_t launch_ss_nl(const ContigArgs& a, const LaunchShape& s, cudaStream_t st) {
+    return (s.variant & (1 << 15)) ? launch_ss_nlt<n, LPB, true>(a, s, st) : launch_ss_nlt<n, LPB, false>(a, s, st);
+}
+
 template <int n>
 cudaError_t launch_ss_n(const ContigArgs& a, const LaunchShape& s, cudaStream_t st) {
-    switch (s.variant >> 10) {
+    switch ((s.variant >> 10) & 31) {
         case 2: return launch_ss_nl<n, 2>(a, s, st);
         case 4: return launch_ss_nl<n, 4>(a, s, st);
         case 6: return launch_ss_nl<n, 6>(a, s, st);
