@@ -79,3 +79,21 @@ def test_tc_combine_vs_oracle_c3_frames(s, monkeypatch):
     monkeypatch.setenv("HETRECO_COMBINE_TC", "1")
     M = sens(s, Y, S)
     assert relmax(M, o.sens_recon(Y, S)) <= TOL
+
+
+@pytest.mark.parametrize("ny,nc,nf,shift", [(256, 32, 12, False), (256, 12, 13, True), (128, 8, 9, False)])
+def test_ss_shared_twiddles_bitexact(s, monkeypatch, ny, nc, nf, shift):
+    """HETRECO_SS_TWSMEM=1: the staged-map combine reading its pass-1 twiddles
+    from a shared table is bit-identical to the register-twiddle kernel (same
+    products, same order) and within tolerance of the reference chain."""
+    rng = np.random.default_rng(ny + 3 * nc + nf)
+    Y = cplx(rng, 256, ny, nc, nf)
+    S = cplx(rng, 256, ny, nc)
+    monkeypatch.setenv("HETRECO_COMBINE_CP", "0")
+    monkeypatch.setenv("HETRECO_SS_TWSMEM", "1")
+    M1 = sens(s, Y, S, {"shift": shift})
+    monkeypatch.setenv("HETRECO_SS_TWSMEM", "0")
+    M0 = sens(s, Y, S, {"shift": shift})
+    assert np.array_equal(M1, M0)
+    if not shift:
+        assert relmax(M1, o.sens_recon(Y, S)) <= TOL
