@@ -22,6 +22,7 @@
 #include <string>
 #include <string_view>
 #include <unordered_map>
+#include <unordered_set>
 #include <vector>
 
 #include "hetreco_b200/data.hpp"
@@ -246,6 +247,10 @@ private:
     // host copies of small buffers uploaded whole (layout headers): execute()
     // of the fused kernels reads the shapes without a device round trip
     std::unordered_map<BufferId, std::vector<std::byte>> shadow_;
+    // buffers whose device bytes may have been written by device work (kernel
+    // outputs, D2D copy targets, raw pointers handed out): a partial upload
+    // cannot start a host shadow of them, only a whole-buffer upload can
+    mutable std::unordered_set<BufferId> device_written_;
     LayoutDescriptor header_layout(BufferId header) const;
     std::unique_ptr<detail::FusedReconKernels> fused_;
     // run-time compiled (NVRTC) kernels: "<unit tag>/<name>" -> entry point

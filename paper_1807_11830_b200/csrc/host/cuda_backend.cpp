@@ -161,6 +161,7 @@ void CudaBackend::release(BufferId id) {
     cudaFreeAsync(it->second.ptr, compute_);
     note_work();
     shadow_.erase(id);
+    device_written_.erase(id);
     used_ -= it->second.size;
     bufs_.erase(it);
 }
@@ -188,9 +189,11 @@ void CudaBackend::upload(BufferId id, std::uint64_t off, std::span<const std::by
     if (bytes.empty()) return;
     constexpr std::uint64_t kShadowMax = 4096;  // layout headers are (1 + 11 A) * 8 bytes
     if (b.size <= kShadowMax) {
-        auto& sh = shadow_[id];
-        sh.resize(b.size);  // a fresh buffer is zero-filled, like the device copy
-        std::memcpy(sh.data() + off, bytes.data(), bytes.size());
+        const bool whole = off == 0 && bytes.size() == b.size;
+        auto it = shadow_.find(id);
+        if (it == shadow_.end() && (whole || !device_written_.count(id)))
+            it = shadow_.emplace(id, std::vector<std::byte>(b.size)).first;  // fresh buffers are zero-filled
+        if (it != shadow_.end()) std::memcpy(it->second.data() + off, bytes.data(), bytes.size());
     }
     make_current();
     note_work();
@@ -243,6 +246,7 @@ void CudaBackend::copy(BufferId src, std::uint64_t so, BufferId dst, std::uint64
     make_current();
     note_work();
     shadow_.erase(dst);
+    device_written_.insert(dst);
     ck(cudaMemcpyAsync(static_cast<char*>(d.ptr) + doff, static_cast<const char*>(s.ptr) + so, n,
                        cudaMemcpyDeviceToDevice, compute_),
        "cudaMemcpyAsync(D2D)");
@@ -347,6 +351,9 @@ void* CudaBackend::stage_params(std::span<const std::byte> params) {
 
 void CudaBackend::execute(const CompiledKernel& kernel, const KernelBinding& bind, std::uint64_t gsize) {
     std::lock_guard lk(mu_);
+    // kernels write their output data buffer (the ABI hands them const headers)
+    shadow_.erase(bind.output);
+    device_written_.insert(bind.output);
     cudaKernel_t jit = nullptr;
     if (kernel.unit_name.rfind("nvrtc#", 0) == 0) {
         auto it = jit_.find(kernel.unit_name + "/" + kernel.name);
@@ -410,7 +417,9 @@ void CudaBackend::check(const char* what) const {
 
 void* CudaBackend::device_pointer(BufferId id) const {
     std::lock_guard lk(mu_);
-    return lookup(id).ptr;
+    void* p = lookup(id).ptr;
+    device_written_.insert(id);  // raw device access may write (process outputs)
+    return p;
 }
 
 std::uint64_t CudaBackend::buffer_size(BufferId id) const {

@@ -113,6 +113,40 @@ def test_backend_capacity_and_ranges():
     b.close()
 
 
+def test_header_shadow_after_device_writes(s):
+    """The backend keeps host shadows of uploaded layout headers so the fused
+    layer-1 kernels read their shapes without a device round trip.  A header
+    buffer last written by the device (D2D copy) and then patched by a partial
+    upload must be read back from the device, not from a zero-assumed shadow."""
+    rng = np.random.default_rng(5)
+    nx, ny, nc, nf = 64, 32, 3, 2
+    Y = cplx(rng, nx, ny, nc, nf)
+    S = cplx(rng, nx, ny, nc)
+    hk = s.register_data(h.Data([Y, S], h.DataKind.KData))
+    ho = s.allocate_data([((nx, ny, nf), np.complex64)])
+    hin, hout = s.fetch_header_bytes(hk), s.fetch_header_bytes(ho)
+    b = h.CudaBackend(0)
+    lay = s.layout_of(hk)
+    data = b.allocate(lay.total_bytes)
+    for arr, rec in zip((Y, S), lay.records):
+        b.upload(data, rec.offset_bytes, np.asfortranarray(arr).reshape(-1, order="F").view(np.uint8))
+    staging = b.allocate(len(hin))
+    b.upload(staging, 0, hin)                 # whole upload: shadowed
+    hdr = b.allocate(len(hin))
+    b.copy(staging, 0, hdr, 0, len(hin))      # device-written: no shadow
+    b.upload(hdr, 0, hin[:8])                 # partial patch (same record count)
+    out = b.allocate(nx * ny * nf * 8)
+    ohdr = b.allocate(len(hout))
+    b.upload(ohdr, 0, hout)
+    b.execute("sens_recon", data, hdr, out, ohdr, b"", nx * ny * nf)
+    b.synchronize()
+    M = np.frombuffer(b.download(out, 0, nx * ny * nf * 8), np.complex64).reshape((nx, ny, nf), order="F")
+    assert relmax(M, o.sens_recon(Y, S)) <= TOL
+    b.close()
+    s.release_data(hk)
+    s.release_data(ho)
+
+
 def test_builtin_registry(s):
     assert set(s.kernel_names()) == {"negate", "fft_radix2_pass", "complex_element_prod", "ximage_sum",
                                      "rss_combine", "matrix_add", "sens_recon", "rss_recon"}
