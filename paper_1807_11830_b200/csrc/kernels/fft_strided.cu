@@ -301,7 +301,13 @@ cudaError_t strided_go(int dir, bool sq, const StridedArgs& a, const LaunchShape
     }
     if constexpr (N == 256 && RQ == 16) {
         if (sq && (s.variant & 64)) {
-            return tma_ring_launch<256, 16, 2, 32>(dir, a, s, tiles, st);
+            switch ((s.variant >> 3) & 7) {  // stages; columns per tile from the block size
+                case 3: return tma_ring_launch<256, 16, 3, 16>(dir, a, s, tiles, st);
+                case 4: return tma_ring_launch<256, 16, 4, 16>(dir, a, s, tiles, st);
+                default:
+                    return s.block == 16 * 16 ? tma_ring_launch<256, 16, 2, 16>(dir, a, s, tiles, st)
+                                              : tma_ring_launch<256, 16, 2, 32>(dir, a, s, tiles, st);
+            }
         }
     }
     if constexpr (N == 512 && RQ == 8) {
@@ -389,11 +395,26 @@ LaunchShape plan_strided(std::uint64_t N, std::uint64_t nx, std::uint64_t planes
     const std::uint64_t tiles = (nx / tx) * planes;
     int occ = 1;
     if (N == 256 && R == 16 && nx == 256 && ring_stages() && !few_tiles && tma_ring_enabled(256)) {
-        s.variant = 64 | (2 << 3);
-        s.block = 32 * T;
-        s.smem = tma_ring_smem<256, 16, 2, 32>();
-        occ = tma_ring_occ<256, 16, 2, 32>(s.block, s.smem);
-        s.grid = int(std::min<std::uint64_t>((nx / 32) * planes, std::uint64_t(sms) * occ));
+        // stages x columns: 2 x 32 (default), or 16-column tiles with 2-4
+        // stages (HETRECO_TMA_STAGES256 = 2|3|4 with HETRECO_TMA_TX256 = 16)
+        const int k = env_int("HETRECO_TMA_STAGES256", 2), ttx = env_int("HETRECO_TMA_TX256", 32);
+        const int K = (ttx == 16 && k >= 2 && k <= 4) ? k : 2, TXc = (ttx == 16) ? 16 : 32;
+        s.variant = 64 | (K << 3);
+        s.block = TXc * T;
+        if (TXc == 32) {
+            s.smem = tma_ring_smem<256, 16, 2, 32>();
+            occ = tma_ring_occ<256, 16, 2, 32>(s.block, s.smem);
+        } else if (K == 2) {
+            s.smem = tma_ring_smem<256, 16, 2, 16>();
+            occ = tma_ring_occ<256, 16, 2, 16>(s.block, s.smem);
+        } else if (K == 3) {
+            s.smem = tma_ring_smem<256, 16, 3, 16>();
+            occ = tma_ring_occ<256, 16, 3, 16>(s.block, s.smem);
+        } else {
+            s.smem = tma_ring_smem<256, 16, 4, 16>();
+            occ = tma_ring_occ<256, 16, 4, 16>(s.block, s.smem);
+        }
+        s.grid = int(std::min<std::uint64_t>((nx / std::uint64_t(TXc)) * planes, std::uint64_t(sms) * occ));
         return s;
     }
     if (N == 512 && R == 8 && nx == 512 && ring_stages() && !few_tiles && tma_ring_enabled(512)) {
