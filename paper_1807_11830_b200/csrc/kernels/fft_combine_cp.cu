@@ -52,17 +52,14 @@ constexpr int cp_groups() {  // coil groups per CTA: ~128 threads
     return T >= 128 ? 1 : 128 / T;
 }
 
-// Resident-CTA floor (a 128-register cap) for the 20-point lines of 5*2^k
-// SENSE: uncapped they take 254 registers (2 CTAs/SM).  Measured at C3 shapes
-// (profiles/round1_combine.md): 160^2 160 -> 150 us; the cap slows RSS and the
-// 12-point 3*2^k lines, which keep the default.
-template <int N, int MODE>
-constexpr int cp_min_blocks() {
-    return (odd_part(N) == 5 && MODE == int(Combine::Sense)) ? 4 : 0;
-}
-
+// No resident-CTA floor: a 128-register cap (4 CTAs/SM) once made the 20-point
+// 5*2^k SENSE lines faster (160^2: 160 -> 150 us, profiles/round1_combine.md)
+// while their exchanges ran 3.4x over the ideal shared-memory wavefronts; with
+// the conflict-free mixed-radix layout (fft_core.cuh pad, row_stride) the
+// uncapped kernel is the faster one (150 -> 106 us,
+// profiles/round2_mixed_radix.md).
 template <int N, int MODE, int G>
-__global__ void __launch_bounds__(G * LineFFT<N>::T, cp_min_blocks<N, MODE>()) k_fft_combine_cp(ContigArgs a, std::uint32_t items) {
+__global__ void __launch_bounds__(G * LineFFT<N>::T) k_fft_combine_cp(ContigArgs a, std::uint32_t items) {
     pdl_launch_dependents();
     using L = LineFFT<N>;
     constexpr int R = L::R, T = L::T;
@@ -70,7 +67,7 @@ __global__ void __launch_bounds__(G * LineFFT<N>::T, cp_min_blocks<N, MODE>()) k
     extern __shared__ float2 smem[];
     const int tid = threadIdx.x;
     const int j = tid % T, g = tid / T;
-    float2* line = smem + g * line_stride<N>();
+    float2* line = smem + g * row_stride<N>();
     const unsigned mask = group_mask<T>(tid);
     typename L::Twiddles tw;
     L::load_twiddles(tw, a.tw, j, a.scale);
@@ -121,7 +118,7 @@ __global__ void __launch_bounds__(G * LineFFT<N>::T, cp_min_blocks<N, MODE>()) k
         for (int p = tid; p < N; p += G * T) {
             float re = 0.f, im = 0.f;
             for (int q = 0; q < G; ++q) {
-                const float2 w = smem[q * line_stride<N>() + L::pad(p)];
+                const float2 w = smem[q * row_stride<N>() + L::pad(p)];
                 re += w.x;
                 im += w.y;
             }
@@ -147,7 +144,7 @@ LaunchShape plan_cp_n(Combine mode, std::uint64_t items, int sms) {
         constexpr int G = cp_groups<n>();
         s.rq = LineFFT<n>::R;
         s.block = G * LineFFT<n>::T;
-        s.smem = G * line_stride<n>() * 8;
+        s.smem = G * row_stride<n>() * 8;
         const int occ = mode == Combine::Sense ? cp_occ<n, 1>(s.smem) : cp_occ<n, 2>(s.smem);
         s.grid = int(std::min<std::uint64_t>(items, std::uint64_t(sms) * occ));
         s.variant = 128;

@@ -63,11 +63,11 @@ __global__ void __launch_bounds__(LPB * LineFFT<N>::T) k_fft_combine_ss(ContigAr
     constexpr int R = L::R, T = L::T, NT = LPB * T;
     constexpr int NS = (N + NT - 1) / NT;  // map elements staged per thread
     extern __shared__ float2 smem[];
-    float2* sbuf = smem + LPB * line_stride<N>();  // 2 x [N]
+    float2* sbuf = smem + LPB * row_stride<N>();  // 2 x [N]
     float2* twt = sbuf + 2 * N;                    // TWS: [T][R - 1]
     const int tid = threadIdx.x;
     const int j = tid % T, l = tid / T;
-    float2* line = smem + l * line_stride<N>();
+    float2* line = smem + l * row_stride<N>();
     typename L::Twiddles tw;
     if constexpr (TWS) {
         static_assert(tws_ok<N>(), "shared pass twiddles need a 2-pass plan with R = T");
@@ -151,7 +151,7 @@ __global__ void __launch_bounds__(LPB * LineFFT<N>::T) k_fft_combine_ss(ContigAr
 
 template <int N, int LPB, bool TWS>
 constexpr int ss_smem() {
-    return (LPB * line_stride<N>() + 2 * N + (TWS ? tws_len<N>() : 0)) * 8;
+    return (LPB * row_stride<N>() + 2 * N + (TWS ? tws_len<N>() : 0)) * 8;
 }
 
 template <int n, int LPB, bool TWS>

@@ -70,10 +70,10 @@ __global__ void __launch_bounds__(LPB * LineFFT<N>::T)
     extern __shared__ __align__(128) float2 sm[];
     float2* ring = sm;                              // K x [LPB rows][N]
     float2* xch = sm + K * TILE;                    // LPB exchange lines
-    const std::uint32_t bars = smem_addr(xch + LPB * line_stride<N>());
+    const std::uint32_t bars = smem_addr(xch + LPB * row_stride<N>());
     const int tid = threadIdx.x;
     const int j = tid % T, l = tid / T;
-    float2* line = xch + l * line_stride<N>();
+    float2* line = xch + l * row_stride<N>();
     typename L::Twiddles tw;
     L::load_twiddles(tw, a.tw, j, a.scale);
     pdl_wait();  // twiddle tables are init-time constants
@@ -160,7 +160,7 @@ __global__ void __launch_bounds__(LPB * LineFFT<N>::T)
 
 template <int N, int MODE, int LPB, int K>
 constexpr int tma_smem() {
-    return (K * LPB * N + LPB * line_stride<N>()) * 8 + K * 8;
+    return (K * LPB * N + LPB * row_stride<N>()) * 8 + K * 8;
 }
 
 template <int N, int MODE, int K>

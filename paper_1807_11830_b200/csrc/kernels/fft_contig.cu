@@ -45,7 +45,7 @@ LaunchShape plan_contig(std::uint64_t N, Combine mode, std::uint64_t items, int 
     const int min_lpb = std::max(1, 32 / T);
     while (lpb > min_lpb && (items + lpb - 1) / lpb < std::uint64_t(2 * sms)) lpb >>= 1;
     s.block = lpb * T;
-    s.smem = lpb * stride_of(N) * 8;
+    s.smem = lpb * row_stride_of(N) * 8;
     int occ = 1;
     if (mode == Combine::None) {
         switch (N) {

@@ -299,9 +299,23 @@ struct LineFFT {
     };
     using Twiddles = std::conditional_t<kTableTw, TableTwiddles, RegTwiddles>;
 
-    // Padded shared-memory index: one 8-byte pad per 16 samples.
-    __device__ __forceinline__ static int pad(int p) { return p + (p >> 4); }
-    static constexpr int padded_len = N + (N >> 4);
+    // Shared-memory index of line position p.  Powers of two: one 8-byte pad
+    // per 16 samples (their exchange strides are powers of two).  Mixed radix
+    // 96 / 160 / 320: no pad -- their strides (5, 20, 80 ... at 160) already
+    // spread over the banks, and the inter-line offset is chosen by the line
+    // stride instead (row_stride<N>(), fft_kernels.cuh; the model is
+    // scripts/tools/bank_sim.py).  192 and 384 keep the pad: unpadded they
+    // have fewer bank conflicts too, but ptxas then schedules their combine
+    // with ~60 fewer registers and fewer loads in flight, and it runs slower
+    // (profiles/round2_mixed_radix.md).
+    static constexpr bool kPadded = !is_mixed_size(N) || N == 192 || N == 384;
+    __device__ __forceinline__ static int pad(int p) {
+        if constexpr (kPadded)
+            return p + (p >> 4);
+        else
+            return p;
+    }
+    static constexpr int padded_len = kPadded ? N + (N >> 4) : N;
 
     // Loads this thread's pass twiddles from the W_N^t table (DIR applied).
     // The last pass' twiddles are pre-multiplied by `scale` so run() applies

@@ -47,9 +47,27 @@ struct IndexSplit {
     }
 };
 
+// Line stride (float2) when a warp's lanes run across lines (column tiles of
+// the axis-1 kernels: lane = line + TX * thread): odd, so consecutive lines
+// start on different banks.
 template <int N>
 constexpr int line_stride() {
     return (LineFFT<N>::padded_len) | 1;  // odd: spreads lines over banks
+}
+
+// Line stride when a warp holds 32/T whole lines (lines-major: lane = line * T
+// + thread; the axis-0, combine and expand kernels).  Powers of two: as
+// line_stride.  Mixed radix with T <= 8 threads per line (96, 160): the first
+// stride >= N that is 8 mod 16, which puts the 4 lines of a warp on
+// complementary bank halves; with an odd stride the lines collide
+// (scripts/tools/bank_sim.py at 160: 624 -> 288 wavefronts per exchange round,
+// ideal 240).
+template <int N>
+constexpr int row_stride() {
+    if constexpr (!is_mixed_size(N) || LineFFT<N>::T > 8)
+        return line_stride<N>();
+    else
+        return N + (24 - N % 16) % 16;
 }
 
 // ---- axis 1 ------------------------------------------------------------------------------
@@ -149,7 +167,7 @@ __global__ void __launch_bounds__(256) k_fft_contig(ContigArgs a, int lpb, std::
     extern __shared__ float2 smem[];
     const int tid = threadIdx.x;
     const int j = tid % T, l = tid / T;
-    float2* line = smem + l * line_stride<N>();
+    float2* line = smem + l * row_stride<N>();
     typename L::Twiddles tw;
     L::load_twiddles(tw, a.tw, j, a.scale);
     pdl_wait();  // twiddle tables are init-time constants
@@ -188,7 +206,7 @@ __global__ void __launch_bounds__(MINB > 1 ? 128 : 256, MINB > 1 ? MINB : 0) k_f
     extern __shared__ float2 smem[];
     const int tid = threadIdx.x;
     const int j = tid % T, l = tid / T;
-    float2* line = smem + l * line_stride<N>();
+    float2* line = smem + l * row_stride<N>();
     typename L::Twiddles tw;
     L::load_twiddles(tw, a.tw, j, a.scale);
     pdl_wait();  // twiddle tables are init-time constants
@@ -358,6 +376,16 @@ inline int stride_of(std::uint64_t N) {
     switch (N) {
 #define X(n) \
     case n: return line_stride<n>();
+        HETRECO_FFT_SIZES(X)
+#undef X
+    }
+    return 0;
+}
+
+inline int row_stride_of(std::uint64_t N) {
+    switch (N) {
+#define X(n) \
+    case n: return row_stride<n>();
         HETRECO_FFT_SIZES(X)
 #undef X
     }

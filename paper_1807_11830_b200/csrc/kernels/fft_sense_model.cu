@@ -31,7 +31,7 @@ __global__ void __launch_bounds__(256) k_fft_expand(ContigArgs a, int lpb, std::
     extern __shared__ float2 smem[];
     const int tid = threadIdx.x;
     const int j = tid % T, l = tid / T;
-    float2* line = smem + l * line_stride<N>();
+    float2* line = smem + l * row_stride<N>();
     typename L::Twiddles tw;
     L::load_twiddles(tw, a.tw, j, 1.0f);
     pdl_wait();  // twiddle tables are init-time constants
@@ -147,7 +147,7 @@ LaunchShape plan_expand(std::uint64_t N, std::uint64_t items, int sms) {
     const int min_lpb = std::max(1, 32 / T);
     while (lpb > min_lpb && (items + lpb - 1) / lpb < std::uint64_t(2 * sms)) lpb >>= 1;
     s.block = lpb * T;
-    s.smem = lpb * stride_of(N) * 8;
+    s.smem = lpb * row_stride_of(N) * 8;
     int occ = 1;
     switch (N) {
 #define X(n) \
