@@ -78,10 +78,11 @@ constexpr int row_stride() {
 // 64-bit division is an emulated call on the GPU).
 
 // MINB > 1 asks ptxas for MINB resident 256-thread CTAs per SM (register cap).
-template <int N, int DIR, int NXC, int RQ = default_points(N), bool PFS = false, int MINB = 1>
-__global__ void __launch_bounds__(MINB > 1 ? 256 : 512, MINB > 1 ? MINB : 0) k_fft_strided(StridedArgs a, int tx, std::uint32_t ntiles) {
+// TWR: pass twiddles in registers also for mixed radix (default: table).
+template <int N, int DIR, int NXC, int RQ = default_points(N), bool PFS = false, int MINB = 1, bool TWR = false>
+__global__ void __launch_bounds__((MINB > 1 || TWR) ? 256 : 512, MINB > 1 ? MINB : 0) k_fft_strided(StridedArgs a, int tx, std::uint32_t ntiles) {
     pdl_launch_dependents();
-    using L = LineFFT<N, RQ>;
+    using L = LineFFT<N, RQ, !is_mixed_size(N) || TWR>;
     constexpr int R = L::R, T = L::T;
     extern __shared__ float2 smem[];
     const int tid = threadIdx.x;

@@ -275,6 +275,21 @@ int strided_occ(int block, int smem, int variant) {
     // them the shared-memory attribute too
     blocks_per_sm(k_fft_strided<N, -1, 0, RQ>, block, smem);
     blocks_per_sm(k_fft_strided<N, 1, 0, RQ>, block, smem);
+    if constexpr (is_mixed_size(N)) {
+        // both directions: blocks_per_sm also sets the shared-memory attribute
+        if (variant & 256) {
+            if (variant & 1) {
+                blocks_per_sm(k_fft_strided<N, -1, N, RQ, true, 1, true>, block, smem);
+                return blocks_per_sm(k_fft_strided<N, 1, N, RQ, true, 1, true>, block, smem);
+            }
+            blocks_per_sm(k_fft_strided<N, -1, N, RQ, false, 1, true>, block, smem);
+            return blocks_per_sm(k_fft_strided<N, 1, N, RQ, false, 1, true>, block, smem);
+        }
+        if (variant & 1) {
+            blocks_per_sm(k_fft_strided<N, -1, N, RQ, true>, block, smem);
+            return blocks_per_sm(k_fft_strided<N, 1, N, RQ, true>, block, smem);
+        }
+    }
     if constexpr (has_variants<N>()) {
         if ((variant & 2) && !(variant & 1)) {
             blocks_per_sm(k_fft_strided<N, -1, N, RQ, false, 3>, block, smem);
@@ -308,6 +323,25 @@ cudaError_t strided_go(int dir, bool sq, const StridedArgs& a, const LaunchShape
                     return s.block == 16 * 16 ? tma_ring_launch<256, 16, 2, 16>(dir, a, s, tiles, st)
                                               : tma_ring_launch<256, 16, 2, 32>(dir, a, s, tiles, st);
             }
+        }
+    }
+    if constexpr (is_mixed_size(N)) {
+        // mixed-radix experiment bits (HETRECO_STRIDED_MIXED): 1 = next-tile
+        // prefetch, 256 = pass twiddles in registers
+        if (sq && (s.variant & 256)) {
+            if (s.variant & 1) {
+                if (dir > 0) k_fft_strided<N, 1, N, RQ, true, 1, true><<<s.grid, s.block, s.smem, st>>>(a, tx, tiles);
+                else k_fft_strided<N, -1, N, RQ, true, 1, true><<<s.grid, s.block, s.smem, st>>>(a, tx, tiles);
+            } else {
+                if (dir > 0) k_fft_strided<N, 1, N, RQ, false, 1, true><<<s.grid, s.block, s.smem, st>>>(a, tx, tiles);
+                else k_fft_strided<N, -1, N, RQ, false, 1, true><<<s.grid, s.block, s.smem, st>>>(a, tx, tiles);
+            }
+            return cudaSuccess;
+        }
+        if (sq && (s.variant & 1)) {
+            if (dir > 0) k_fft_strided<N, 1, N, RQ, true><<<s.grid, s.block, s.smem, st>>>(a, tx, tiles);
+            else k_fft_strided<N, -1, N, RQ, true><<<s.grid, s.block, s.smem, st>>>(a, tx, tiles);
+            return cudaSuccess;
         }
     }
     if constexpr (N == 512 && RQ == 8) {
@@ -387,11 +421,15 @@ LaunchShape plan_strided(std::uint64_t N, std::uint64_t nx, std::uint64_t planes
         while (tx_default > 8 && (nx / std::uint64_t(tx_default)) * planes < std::uint64_t(sms)) tx_default >>= 1;
         s.variant = env_int("HETRECO_STRIDED_PF", 0);
     }
+    // mixed radix, square: next-tile prefetch + pass twiddles in registers
+    // (bits 1 | 256; measured 3-21 % faster at 96..320, profiles/round2_mixed_radix.md)
+    if (mixed && nx == N) s.variant = env_int("HETRECO_STRIDED_MIXED", 257);
     if (const int e = env_int("HETRECO_STRIDED_TX", tx_default)) tx = std::uint64_t(e);
     tx = std::min<std::uint64_t>(tx, nx);
     while (tx > 1 && nx % tx) tx >>= 1;  // both powers of two in practice
     s.block = int(tx) * T;
     s.smem = int(tx) * ls_bytes;
+    if ((s.variant & 256) && (!mixed || s.block > 256)) s.variant &= ~256;  // register twiddles: <= 256 threads
     const std::uint64_t tiles = (nx / tx) * planes;
     int occ = 1;
     if (N == 256 && R == 16 && nx == 256 && ring_stages() && !few_tiles && tma_ring_enabled(256)) {

@@ -48,7 +48,7 @@ def np_sens(Y, S):
 
 
 @pytest.mark.parametrize("shape", [(160, 160, 3), (96, 160, 2), (192, 96, 1), (320, 320, 1), (384, 64, 2),
-                                   (160, 256, 2), (64, 320, 1)])
+                                   (160, 256, 2), (64, 320, 1), (384, 384, 2), (96, 96, 3), (192, 192, 2)])
 @pytest.mark.parametrize("direction", ["forward", "inverse"])
 def test_fft2d_mixed_vs_numpy(s, shape, direction):
     rng = np.random.default_rng(sum(shape))
@@ -71,7 +71,8 @@ def test_fft2d_mixed_shift_and_rejections(s):
         run(s, "fft2d", [cplx(rng, 100, 100)], (100, 100))
 
 
-@pytest.mark.parametrize("nx,ny,nc,nf", [(160, 160, 8, 4), (96, 192, 4, 2), (320, 160, 3, 1)])
+@pytest.mark.parametrize("nx,ny,nc,nf", [(160, 160, 8, 4), (96, 192, 4, 2), (320, 160, 3, 1), (96, 96, 5, 3),
+                                        (192, 192, 4, 2), (320, 320, 3, 2), (384, 384, 2, 2)])
 @pytest.mark.parametrize("shift", [False, True])
 def test_recon_mixed_vs_numpy(s, nx, ny, nc, nf, shift):
     rng = np.random.default_rng(nx + ny + nc)
