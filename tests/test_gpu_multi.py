@@ -130,3 +130,25 @@ def test_one_context_per_process():
     assert r.returncode == 0, r.stderr
     n, before, after = map(int, r.stdout.split()[-3:])
     assert n >= 1 and before == 0 and after == 1, r.stdout
+
+
+def test_bench_two_ranks_on_one_gpu():
+    """The multi-rank bench path (torchrun, one process per rank, frame slabs of
+    one C3 volume, no data-path collective) as a dry run: two ranks pinned to
+    GPU 0 with gloo carrying only the barrier and the max-over-ranks timing."""
+    import json
+    import os
+    env = dict(os.environ, HETRECO_BENCH_DEVICE="0", HETRECO_BENCH_DIST="gloo")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", "29531", os.path.join(ROOT, "bench.py"),
+           "--gpus", "2", "--steps", "3", "--warmup", "3", "--no-extras", "--no-cpu-baseline",
+           "--no-session-flow", "--no-weak"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [json.loads(x) for x in r.stdout.splitlines() if x.startswith("{")]
+    assert len(lines) == 1, r.stdout  # rank 0 alone prints
+    b = lines[0]
+    assert b["n_gpus"] == 2 and b["scaling"] == "strong" and b["value"] > 0
+    assert b["sharding"]["frames_per_gpu"] == [15, 15]
+    assert b["e2e"]["matches_resident"] is True
+    assert b["config"]["parallelism"].startswith("frame-slab x2")
