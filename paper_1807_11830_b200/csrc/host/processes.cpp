@@ -1179,9 +1179,13 @@ public:
             s_col_ = dev::plan_strided_masked(ny_, normal_, nc_ * nf_, sms);
         }
         fused_ = dev::LaunchShape{};
+        front_clusters_ = 0;
         if (normal_) {
             tw_inv_ = twiddle_table(nx_, +1);
             fused_ = dev::plan_sense_normal_fused(nx_, nc_ * nf_, sms);
+            // expand + x-FFT + y-FFT/mask/y-IFFT as one 16-CTA-cluster kernel at
+            // 256^2 (fft_sense_cluster.cu; opt-in HETRECO_NORMAL_CLUSTER=1, measured slower)
+            front_clusters_ = fused_.block ? 0 : dev::plan_sense_front(nx_, ny_, nc_ * nf_);
             if (scratch_.size() != nx_ * ny_ * nc_ * nf_ * 8) scratch_ = DevMem(nx_ * ny_ * nc_ * nf_ * 8);
             s_comb_ = dev::combine_cp_preferred(nx_, ny_ * nf_, nc_, sms)
                           ? dev::plan_combine_cp(nx_, dev::Combine::Sense, ny_ * nf_, sms)
@@ -1205,6 +1209,17 @@ public:
                                     float(1.0 / (double(nx_) * double(ny_)))};
             an.phases = int(env_or("HETRECO_NORMAL_PHASES", 7));
             ck(dev::launch_sense_normal_fused(nx_, an, fused_, s), name() + "/normal-fused");
+            mark(s);
+            return;
+        }
+        if (normal_ && front_clusters_ > 0) {
+            dev::SenseFrontArgs af{m_, s_, mask_, z, tw_fwd_.as<float2>(), std::uint32_t(nc_), std::uint32_t(nf_),
+                                   shift_, 1.0f};
+            ck(dev::launch_sense_front(af, front_clusters_, s), name() + "/expand.x-fft.y-fft.mask.y-ifft (cluster)");
+            mark(s);
+            dev::ContigArgs ar{z, out_, s_, ny_, nc_, nf_, shift_, shift_, float(1.0 / (double(nx_) * double(ny_))),
+                               tw_inv_.as<float2>()};
+            ck(dev::launch_contig(nx_, +1, dev::Combine::Sense, ar, s_comb_, s), name() + "/x-ifft+combine");
             mark(s);
             return;
         }
@@ -1238,6 +1253,7 @@ private:
     float2* out_ = nullptr;
     DevMem tw_fwd_, tw_fwd_y_, tw_inv_, scratch_;
     dev::LaunchShape s_exp_, s_col_, s_comb_, fused_;
+    int front_clusters_ = 0;
     bool generic_cols_ = false;
 };
 

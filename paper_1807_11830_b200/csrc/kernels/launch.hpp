@@ -195,6 +195,26 @@ cudaError_t launch_cluster(Combine mode, const ClusterMap& m, const ClusterLaunc
 
 // ---- SENSE forward model E = P F S and normal operator E^H E ----
 
+// Normal-operator front half at 256 x 256 on 16-CTA clusters
+// (fft_sense_cluster.cu): out[:, :, c, f] = F_y^-1 P F_y F_x (S_c . M_f), the
+// output of launch_expand + launch_strided_masked(roundtrip), bit-identical.
+struct SenseFrontArgs {
+    const float2* m;     // M [256, 256, F]
+    const float2* smap;  // S [256, 256, C]
+    const float* mask;   // P [256, 256] or null
+    float2* out;         // [256, 256, C, F]
+    const float2* tw;    // forward W_256^t
+    std::uint32_t coils, frames;
+    int shift;
+    float scale;  // applied at the store (1 in the normal operator)
+};
+// Clusters to launch (<= coil images), 0 when the kernel does not apply
+// (size; opt-in with HETRECO_NORMAL_CLUSTER=1, measured slower) or cannot run
+// on this device.
+int plan_sense_front(std::uint64_t nx, std::uint64_t ny, std::uint64_t coil_images);
+cudaError_t launch_sense_front(const SenseFrontArgs& a, int clusters, cudaStream_t stream);
+
+
 // Expand + forward axis-0 FFT: out line (y, c, f) = F_x( S[:, y, c] * M[:, y, f] ).
 // a.in = M [N, ny, F], a.smap = S [N, ny, C], a.out = [N, ny, C, F].
 LaunchShape plan_expand(std::uint64_t N, std::uint64_t items /* ny*C*F */, int device_sms);

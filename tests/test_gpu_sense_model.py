@@ -137,3 +137,21 @@ def test_sense_normal_fused_cooperative(s, monkeypatch, n, nc, nf, points):
     mask = np.asfortranarray((rng.random((n, n)) < 0.4).astype(np.float32))
     out, *_ = run(s, "sense_normal", [M, S, mask], (n, n, nf))
     assert relmax(out, o.sense_normal(M, S, mask)) <= TOL
+
+
+@pytest.mark.parametrize("nc,nf,shift,masked", [(8, 1, False, True), (8, 1, True, True), (3, 2, False, False),
+                                                (20, 1, True, True)])
+def test_sense_normal_cluster_front_bitexact(s, monkeypatch, nc, nf, shift, masked):
+    """HETRECO_NORMAL_CLUSTER=1 (fft_sense_cluster.cu): expand, x-FFT, DSMEM
+    transpose and the masked y round trip in one 16-CTA-cluster kernel, bit-
+    identical to the two-kernel front (20 coil images exceed the resident
+    clusters, so clusters loop over images)."""
+    rng = np.random.default_rng(nc * 10 + nf)
+    M = cplx(rng, 256, 256, nf)
+    S = cplx(rng, 256, 256, nc)
+    inputs = [M, S] + ([np.asfortranarray((rng.random((256, 256)) < 0.4).astype(np.float32))] if masked else [])
+    monkeypatch.setenv("HETRECO_NORMAL_CLUSTER", "1")
+    a = run(s, "sense_normal", inputs, (256, 256, nf), {"shift": shift})[0]
+    monkeypatch.delenv("HETRECO_NORMAL_CLUSTER")
+    b = run(s, "sense_normal", inputs, (256, 256, nf), {"shift": shift})[0]
+    assert np.array_equal(a, b)
