@@ -237,7 +237,7 @@ def run_ours(args):
     all_cpus = os.sched_getaffinity(0)
     numa_node = h.bind_to_device_numa(local)
     devs = h.enumerate_devices()  # descriptors only: no context on the other GPUs
-    s = h.ComputeSession(device=devs[local])
+    s = h.ComputeSession(device=next(d for d in devs if d.backend_id == f"cuda{local}"))
     # strong scaling: one 30-frame volume, rank r owns frames [b, e)
     fb, fe = frame_slab(rank, world, NF)
     nfr = fe - fb
