@@ -81,11 +81,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_sense_normal_front(SenseFrontAr
     LS::load_twiddles(tw1, a.tw, j1, 1.0f);
     LS::load_twiddles(tw2, a.tw, j2, 1.0f);
     const std::uint32_t col = r * kRows + std::uint32_t(l2);
-    if (tid == 0) {
-        mbar_init(rbar, 1);
-        mbar_expect_tx(rbar, kRecvBytes);
-    }
-    __syncthreads();
+    if (tid == 0) mbar_init(rbar, 1);
+    __syncthreads();  // the initialised barrier is visible to every thread before first use
+    if (tid == 0) mbar_expect_tx(rbar, kRecvBytes);
     cluster_arrive();  // every CTA's barrier is armed before any DSMEM store
     cluster_wait();
     pdl_wait();  // inputs may come from the previous kernel
