@@ -41,9 +41,9 @@ public:
     ComputeSession(const ComputeSession&) = delete;
     ComputeSession& operator=(const ComputeSession&) = delete;
 
-    const DeviceDescriptor& device() const { return device_; }
+    const DeviceDescriptor& device() const { return selected_; }
     Backend& backend() { return backend_; }
-    std::uint64_t uid() const { return uid_; }
+    std::uint64_t uid() const { return session_uid_; }
 
     // ---- data (session.hpp:73-90) ----
     DataHandle register_data(const Data& data);
@@ -58,7 +58,7 @@ public:
     void release_data(DataHandle handle);
     const LayoutDescriptor& layout_of(DataHandle handle) const;
     DataKind kind_of(DataHandle handle) const;
-    std::size_t live_data_count() const { return entries_.size(); }
+    std::size_t live_data_count() const { return slots_.size(); }
     std::vector<std::byte> fetch_header_bytes(DataHandle handle);
     void copy_array(DataHandle src, std::size_t src_index, DataHandle dst, std::size_t dst_index);
 
@@ -75,37 +75,37 @@ public:
     // ---- kernels (session.hpp:94-124) ----
     void load_builtin_kernels();
     void load_kernels(std::span<const ProgramSource> units);
-    const KernelRegistry& kernels() const { return registry_; }
+    const KernelRegistry& kernels() const { return kernel_table_; }
     void launch_kernel(std::string_view name, DataHandle input, DataHandle output,
                        std::span<const std::byte> params, std::uint64_t global_size);
     void synchronize();
 
     // ---- accounting ----
-    TransferCounters counters() const { return counters_; }
-    void reset_counters() { counters_ = {}; }
+    TransferCounters counters() const { return transfers_; }
+    void reset_counters() { transfers_ = {}; }
 
 private:
-    struct Entry {
-        BufferId data_buffer = 0;
-        BufferId header_buffer = 0;
+    struct Slot {
+        BufferId payload = 0;
+        BufferId header_buf = 0;
         LayoutDescriptor layout;
         DataKind kind = DataKind::Generic;
     };
-    const Entry& resolve(DataHandle handle) const;
+    const Slot& resolve(DataHandle handle) const;
     // record `index` of a live entry, with `role` naming the side in errors
-    const LayoutRecord& record_of(const Entry& e, std::size_t index, const char* role) const;
-    DataHandle insert(const LayoutDescriptor& layout, DataKind kind, std::span<const void* const> payload);
-    void drop_buffers(const Entry& e) noexcept;
+    const LayoutRecord& record_of(const Slot& e, std::size_t index, const char* role) const;
+    DataHandle insert(const LayoutDescriptor& layout, DataKind kind, std::span<const void* const> host_src);
+    void drop_buffers(const Slot& e) noexcept;
 
     Backend& backend_;
-    DeviceDescriptor device_;
-    std::uint64_t uid_ = 0;
-    std::uint64_t alignment_ = 256;
-    std::uint64_t next_id_ = 1;
-    std::unordered_map<std::uint64_t, Entry> entries_;
-    KernelRegistry registry_;
-    TransferCounters counters_;
-    bool builtins_loaded_ = false;
+    DeviceDescriptor selected_;
+    std::uint64_t session_uid_ = 0;
+    std::uint64_t pack_alignment_ = 256;
+    std::uint64_t next_handle_id_ = 1;
+    std::unordered_map<std::uint64_t, Slot> slots_;
+    KernelRegistry kernel_table_;
+    TransferCounters transfers_;
+    bool have_builtins_ = false;
 };
 
 }  // namespace hetreco
