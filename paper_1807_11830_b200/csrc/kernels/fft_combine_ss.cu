@@ -36,6 +36,41 @@ __device__ __forceinline__ float2 lds_f2(std::uint32_t addr) {
 // HETRECO_SS_TWSMEM=0|1 (profiles/round2_summary.md).
 bool ss_tws(std::uint64_t N) { return N == 256 && env_int("HETRECO_SS_TWSMEM", 0) == 1; }
 
+// Line exchange by warp shuffles instead of shared memory at 256 points
+// (north_star's "warp-shuffle butterflies"): A/B switch HETRECO_SS_SHFL=1.
+bool ss_shfl(std::uint64_t N) { return N == 256 && env_int("HETRECO_SS_SHFL", 0) == 1; }
+
+// run_f of the 2-pass 256-point plan (16 x 16) with the pass-0 -> pass-1
+// exchange done in registers: the exchange is the 16 x 16 transpose
+// v'[m] (lane j) = v[j] (lane m) among the line's 16 lanes, as four butterfly
+// stages (lane ^ 1, 2, 4, 8), each swapping 8 value pairs; which value of a
+// pair a lane sends depends on its lane bit, hence the selects.
+template <int DIR, class Twiddles>
+__device__ __forceinline__ void run_shfl(float2 (&v)[16], const Twiddles& twd, int j, float scale) {
+    using L = LineFFT<256>;
+    static_assert(L::P == 2 && L::R == 16 && L::T == 16, "256 = 16 x 16");
+    dft_regs<16, DIR, 1, 0>(v);  // pass 0
+    sfor<4>([&](auto sc) {
+        constexpr int d = 1 << sc.value;
+        const bool hi = (j >> sc.value) & 1;
+        sfor<16>([&](auto qc) {
+            constexpr int q = qc.value;
+            if constexpr ((q & d) == 0) {
+                const float2 snd = hi ? v[q] : v[q | d];
+                const float2 rcv = make_float2(__shfl_xor_sync(0xffffffffu, snd.x, d), __shfl_xor_sync(0xffffffffu, snd.y, d));
+                if (hi)
+                    v[q] = rcv;
+                else
+                    v[q | d] = rcv;
+            }
+        });
+    });
+    // pass 1: twiddles (the last pass: pre-scaled), the q = 0 slot scaled, DFT
+    sfor<15>([&](auto qc) { v[qc.value + 1] = cmul(v[qc.value + 1], twd.w[L::tw_offset(1) + qc.value]); });
+    if (scale != 1.0f) v[0] = cscale(v[0], scale);
+    dft_regs<16, DIR, 1, 0>(v);
+}
+
 int ss_lines(std::uint64_t N) {
     const int v = env_int("HETRECO_SS_LINES", N >= 512 ? 2 : 4);
     return (v == 2 || v == 4 || v == 6 || v == 8 || v == 16) ? v : kSsLines;
@@ -55,7 +90,7 @@ constexpr int tws_len() {
     return tws_ok<N>() ? LineFFT<N>::T * (LineFFT<N>::R - 1) : 0;
 }
 
-template <int N, int LPB, bool TWS>
+template <int N, int LPB, int XV>
 __global__ void __launch_bounds__(LPB * LineFFT<N>::T) k_fft_combine_ss(ContigArgs a, std::uint32_t gpy,
                                                                         std::uint32_t groups) {
     pdl_launch_dependents();
@@ -64,6 +99,7 @@ __global__ void __launch_bounds__(LPB * LineFFT<N>::T) k_fft_combine_ss(ContigAr
     constexpr int NS = (N + NT - 1) / NT;  // map elements staged per thread
     extern __shared__ float2 smem[];
     float2* sbuf = smem + LPB * row_stride<N>();  // 2 x [N]
+    constexpr bool TWS = XV == 1, SHF = XV == 2;
     float2* twt = sbuf + 2 * N;                    // TWS: [T][R - 1]
     const int tid = threadIdx.x;
     const int j = tid % T, l = tid / T;
@@ -127,7 +163,9 @@ __global__ void __launch_bounds__(LPB * LineFFT<N>::T) k_fft_combine_ss(ContigAr
                 load_x(c + 1, xn);
                 load_s(c + 1);
             }
-            if constexpr (TWS) {
+            if constexpr (SHF) {
+                run_shfl<+1>(v, tw, j, a.scale);
+            } else if constexpr (TWS) {
                 // volatile shared loads: re-read per coil, never hoisted into registers
                 L::template run_f<+1>(
                     v, [&](auto, auto, auto qc) { return lds_f2(tws_row + 8u * qc.value); }, line, j,
@@ -149,31 +187,32 @@ __global__ void __launch_bounds__(LPB * LineFFT<N>::T) k_fft_combine_ss(ContigAr
     }
 }
 
-template <int N, int LPB, bool TWS>
+template <int N, int LPB, int XV>
 constexpr int ss_smem() {
-    return (LPB * row_stride<N>() + 2 * N + (TWS ? tws_len<N>() : 0)) * 8;
+    return (LPB * row_stride<N>() + 2 * N + (XV == 1 ? tws_len<N>() : 0)) * 8;
 }
 
-template <int n, int LPB, bool TWS>
+template <int n, int LPB, int XV>
 LaunchShape plan_ss_nlt(std::uint64_t ny, std::uint64_t frames, int sms) {
     LaunchShape s;
-    if constexpr (n >= 64 && LPB * LineFFT<n>::T <= 1024 && (!TWS || tws_ok<n>())) {
+    if constexpr (n >= 64 && LPB * LineFFT<n>::T <= 1024 && (XV == 0 || (XV == 1 && tws_ok<n>()) || (XV == 2 && n == 256))) {
         s.rq = LineFFT<n>::R;
         s.block = LPB * LineFFT<n>::T;
-        s.smem = ss_smem<n, LPB, TWS>();
+        s.smem = ss_smem<n, LPB, XV>();
         const std::uint64_t groups = ny * ((frames + LPB - 1) / LPB);
-        const int occ = blocks_per_sm(k_fft_combine_ss<n, LPB, TWS>, s.block, s.smem);
+        const int occ = blocks_per_sm(k_fft_combine_ss<n, LPB, XV>, s.block, s.smem);
         const int per_sm = env_int("HETRECO_SS_CTAS_PER_SM", occ);  // experiments (profiles/round1_combine.md)
         s.grid = int(std::min<std::uint64_t>(groups, std::uint64_t(sms) * std::uint64_t(per_sm > 0 ? per_sm : occ)));
-        s.variant = 256 | (LPB << 10) | (TWS ? (1 << 15) : 0);
+        s.variant = 256 | (LPB << 10) | (XV == 1 ? (1 << 15) : 0) | (XV == 2 ? (1 << 16) : 0);
     }
     return s;
 }
 
 template <int n, int LPB>
 LaunchShape plan_ss_nl(std::uint64_t ny, std::uint64_t frames, int sms) {
-    if (ss_tws(n)) return plan_ss_nlt<n, LPB, true>(ny, frames, sms);
-    return plan_ss_nlt<n, LPB, false>(ny, frames, sms);
+    if (ss_tws(n)) return plan_ss_nlt<n, LPB, 1>(ny, frames, sms);
+    if (ss_shfl(n)) return plan_ss_nlt<n, LPB, 2>(ny, frames, sms);
+    return plan_ss_nlt<n, LPB, 0>(ny, frames, sms);
 }
 
 template <int n>
@@ -187,13 +226,13 @@ LaunchShape plan_ss_n(std::uint64_t ny, std::uint64_t frames, int sms) {
     }
 }
 
-template <int n, int LPB, bool TWS>
+template <int n, int LPB, int XV>
 cudaError_t launch_ss_nlt(const ContigArgs& a, const LaunchShape& s, cudaStream_t st) {
-    if constexpr (n >= 64 && LPB * LineFFT<n>::T <= 1024 && (!TWS || tws_ok<n>())) {
+    if constexpr (n >= 64 && LPB * LineFFT<n>::T <= 1024 && (XV == 0 || (XV == 1 && tws_ok<n>()) || (XV == 2 && n == 256))) {
         const std::uint64_t gpy = (a.frames + LPB - 1) / LPB;
         const std::uint64_t groups = a.ny * gpy;
         if (groups >= (std::uint64_t(1) << 32)) return cudaErrorInvalidValue;
-        k_fft_combine_ss<n, LPB, TWS><<<s.grid, s.block, s.smem, st>>>(a, std::uint32_t(gpy), std::uint32_t(groups));
+        k_fft_combine_ss<n, LPB, XV><<<s.grid, s.block, s.smem, st>>>(a, std::uint32_t(gpy), std::uint32_t(groups));
         return cudaGetLastError();
     } else {
         return cudaErrorInvalidValue;
@@ -202,7 +241,9 @@ cudaError_t launch_ss_nlt(const ContigArgs& a, const LaunchShape& s, cudaStream_
 
 template <int n, int LPB>
 cudaError_t launch_ss_nl(const ContigArgs& a, const LaunchShape& s, cudaStream_t st) {
-    return (s.variant & (1 << 15)) ? launch_ss_nlt<n, LPB, true>(a, s, st) : launch_ss_nlt<n, LPB, false>(a, s, st);
+    if (s.variant & (1 << 15)) return launch_ss_nlt<n, LPB, 1>(a, s, st);
+    if (s.variant & (1 << 16)) return launch_ss_nlt<n, LPB, 2>(a, s, st);
+    return launch_ss_nlt<n, LPB, 0>(a, s, st);
 }
 
 template <int n>

@@ -97,3 +97,18 @@ def test_ss_shared_twiddles_bitexact(s, monkeypatch, ny, nc, nf, shift):
     assert np.array_equal(M1, M0)
     if not shift:
         assert relmax(M1, o.sens_recon(Y, S)) <= TOL
+
+
+@pytest.mark.parametrize("ny,nc,nf,shift", [(256, 32, 12, False), (256, 12, 13, True), (128, 8, 9, False)])
+def test_ss_shuffle_exchange_bitexact(s, monkeypatch, ny, nc, nf, shift):
+    """HETRECO_SS_SHFL=1: the staged-map combine exchanging its 256-point lines
+    by a warp-shuffle transpose is bit-identical to the shared-memory exchange."""
+    rng = np.random.default_rng(ny + 5 * nc + nf)
+    Y = cplx(rng, 256, ny, nc, nf)
+    S = cplx(rng, 256, ny, nc)
+    monkeypatch.setenv("HETRECO_COMBINE_CP", "0")
+    monkeypatch.setenv("HETRECO_SS_SHFL", "1")
+    M1 = sens(s, Y, S, {"shift": shift})
+    monkeypatch.setenv("HETRECO_SS_SHFL", "0")
+    M0 = sens(s, Y, S, {"shift": shift})
+    assert np.array_equal(M1, M0)
