@@ -426,6 +426,7 @@ LaunchShape plan_strided(std::uint64_t N, std::uint64_t nx, std::uint64_t planes
     if (mixed && nx == N) s.variant = env_int("HETRECO_STRIDED_MIXED", 257);
     if (const int e = env_int("HETRECO_STRIDED_TX", tx_default)) tx = std::uint64_t(e);
     tx = std::min<std::uint64_t>(tx, nx);
+    tx = std::min<std::uint64_t>(tx, std::uint64_t(std::max(1, 512 / T)));  // the kernels' 512-thread bound
     while (tx > 1 && nx % tx) tx >>= 1;  // both powers of two in practice
     s.block = int(tx) * T;
     s.smem = int(tx) * ls_bytes;
